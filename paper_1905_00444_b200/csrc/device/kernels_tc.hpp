@@ -1,0 +1,20 @@
+// K2 tensor-core path: complex64 GEMM as a real GEMM on tcgen05 (kind::tf32)
+// with a 3xTF32 split for FP32-level accuracy.  See cgemm_tc.cu.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace qsg::dev {
+
+// True when the shape/layout is handled by the tcgen05 kernel.
+bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
+std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
+cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
+// Process-wide switch (QSG_TENSOR_CORES=0 disables); the engine also has
+// a per-instance option.
+bool tc_enabled();
+
+}  // namespace qsg::dev

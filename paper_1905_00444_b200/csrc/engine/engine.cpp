@@ -1,0 +1,573 @@
+// Device executor: plan -> static device program -> per-slice replay.
+// See engine.hpp for the design; reference behaviour cited inline.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <sstream>
+#include <stdexcept>
+
+#include "../device/kernels_tc.hpp"
+
+namespace qsg {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+constexpr std::int64_t kAlign = 256;
+
+std::int64_t align_up(std::int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+std::vector<std::int64_t> row_major_strides(const std::vector<std::int64_t>& dims) {
+  std::vector<std::int64_t> s(dims.size());
+  std::int64_t acc = 1;
+  for (std::size_t i = dims.size(); i-- > 0;) {
+    s[i] = acc;
+    acc *= dims[i];
+  }
+  return s;
+}
+
+// A tensor as the program sees it at compile time.
+struct View {
+  int buf = -1;
+  std::int64_t off = 0;
+  int node = -1;
+  std::vector<Label> labels;
+  std::vector<std::int64_t> dims;
+  std::vector<std::int64_t> strides;
+  int meta = -1;  // -1: node tensor (never renormalised)
+  std::int64_t volume() const {
+    std::int64_t v = 1;
+    for (auto d : dims) v *= d;
+    return v;
+  }
+  bool dense() const { return strides == row_major_strides(dims); }
+  std::int64_t dim_of(const Label& l) const {
+    for (std::size_t i = 0; i < labels.size(); ++i)
+      if (labels[i] == l) return dims[i];
+    throw std::invalid_argument("execute: no label " + l);
+  }
+  std::int64_t stride_of(const Label& l) const {
+    for (std::size_t i = 0; i < labels.size(); ++i)
+      if (labels[i] == l) return strides[i];
+    throw std::invalid_argument("execute: no label " + l);
+  }
+  bool has(const Label& l) const { return std::find(labels.begin(), labels.end(), l) != labels.end(); }
+};
+
+bool seq_equal(const std::vector<Label>& a, std::size_t a0, const std::vector<Label>& b) {
+  if (a0 + b.size() > a.size()) return false;
+  for (std::size_t i = 0; i < b.size(); ++i)
+    if (a[a0 + i] != b[i]) return false;
+  return true;
+}
+
+}  // namespace
+
+Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOptions& opt)
+    : circuit_(c), plan_(plan), opt_(opt) {
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  // Node layout = fold layout (open label at axis 0, bonds in gate order).
+  std::vector<int> x1(static_cast<std::size_t>(c.num_qubits()), 0);
+  for (int q : plan_.open_qubits) x1[static_cast<std::size_t>(q)] = -1;
+  shape_ = fold_worldlines(c, x1).shape();
+  if (shape_.open_qubits != plan_.open_qubits)
+    throw std::invalid_argument("engine: plan open qubits do not match the circuit fold");
+  batch_ = std::int64_t{1} << plan_.open_qubits.size();
+  compile();
+  pack_buffers();
+  check(cudaMalloc(&arena_, static_cast<std::size_t>(std::max<std::int64_t>(arena_bytes_, kAlign))), "arena cudaMalloc");
+  check(cudaMalloc(&metas_, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta cudaMalloc");
+  check(cudaMemset(metas_, 0, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta memset");
+  check(cudaMalloc(&acc_, sizeof(double2) * static_cast<std::size_t>(batch_)), "acc cudaMalloc");
+  check(cudaMemset(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_)), "acc memset");
+  check(cudaHostAlloc(reinterpret_cast<void**>(&staging_), static_cast<std::size_t>(std::max<std::int64_t>(node_bytes_, 8)),
+                      cudaHostAllocDefault),
+        "pinned staging");
+  op_ms_.assign(ops_.size(), 0.0);
+  op_execs_.assign(ops_.size(), 0);
+  set_profile(opt_.profile);
+}
+
+void Engine::set_profile(bool on) {
+  opt_.profile = on;
+  if (on && ev_.empty()) {
+    check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    ev_.resize(2 * ops_.size());
+    for (auto& e : ev_) check(cudaEventCreate(&e), "cudaEventCreate");
+  }
+}
+
+Engine::~Engine() {
+  cudaSetDevice(opt_.device);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto e : ev_) cudaEventDestroy(e);
+  if (arena_) cudaFree(arena_);
+  if (metas_) cudaFree(metas_);
+  if (acc_) cudaFree(acc_);
+  if (per_slice_) cudaFree(per_slice_);
+  if (staging_) cudaFreeHost(staging_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::compile() {
+  // ---- node region ---------------------------------------------------------
+  const std::size_t n = shape_.nodes.size();
+  node_elem_off_.assign(n, 0);
+  node_vol_.assign(n, 0);
+  node_full_strides_.assign(n, {});
+  node_cut_axes_.assign(n, {});
+  std::int64_t elems = 0;
+  for (std::size_t q = 0; q < n; ++q) {
+    node_elem_off_[q] = elems;
+    node_vol_[q] = shape_.nodes[q].volume();
+    node_full_strides_[q] = row_major_strides(shape_.nodes[q].dims);
+    elems += align_up(node_vol_[q] * 8) / 8;
+  }
+  node_bytes_ = elems * 8;
+  bufs_.clear();
+  ops_.clear();
+  bufs_.push_back(Buffer{node_bytes_, 0, 1 << 30, 0});  // buffer 0: node region, always live
+
+  const std::size_t fixed = cut_fixed_count(shape_, plan_.cut);
+  std::map<std::string, View> live;
+  for (std::size_t q = 0; q < n; ++q) {
+    const auto& node = shape_.nodes[q];
+    View v;
+    v.buf = 0;
+    v.off = node_elem_off_[q];
+    v.node = static_cast<int>(q);
+    std::vector<int> cut_axes(fixed, -1);
+    for (std::size_t a = 0; a < node.labels.size(); ++a) {
+      auto it = std::find(plan_.cut.labels.begin(), plan_.cut.labels.begin() + static_cast<std::ptrdiff_t>(fixed),
+                          node.labels[a]);
+      if (it != plan_.cut.labels.begin() + static_cast<std::ptrdiff_t>(fixed)) {
+        cut_axes[static_cast<std::size_t>(it - plan_.cut.labels.begin())] = static_cast<int>(a);
+        continue;
+      }
+      v.labels.push_back(node.labels[a]);
+      v.dims.push_back(node.dims[a]);
+      v.strides.push_back(node_full_strides_[q][a]);
+    }
+    node_cut_axes_[q] = cut_axes;
+    live[node_name(static_cast<int>(q))] = std::move(v);
+  }
+
+  auto new_buf = [&](std::int64_t bytes) {
+    Buffer b;
+    b.bytes = align_up(std::max<std::int64_t>(bytes, 8));
+    b.first = b.last = static_cast<int>(ops_.size());
+    bufs_.push_back(b);
+    return static_cast<int>(bufs_.size()) - 1;
+  };
+  auto touch = [&](int buf) {
+    if (buf > 0) bufs_[static_cast<std::size_t>(buf)].last = static_cast<int>(ops_.size());
+  };
+  auto as_operand = [](const View& v) { return Operand{v.buf, v.off, v.node}; };
+  // Emits K1 making `v` dense in `order`; returns the new view.
+  auto permute_to = [&](const View& v, const std::vector<Label>& order, int step) {
+    Op op;
+    op.kind = 0;
+    op.step = step;
+    op.src = as_operand(v);
+    View out;
+    out.meta = v.meta;
+    for (const auto& l : order) {
+      op.ext.push_back(v.dim_of(l));
+      op.istr.push_back(v.stride_of(l));
+      out.labels.push_back(l);
+      out.dims.push_back(v.dim_of(l));
+    }
+    out.strides = row_major_strides(out.dims);
+    op.count = out.volume();
+    touch(v.buf);
+    op.dst = new_buf(op.count * 8);
+    out.buf = op.dst;
+    out.off = 0;
+    ops_.push_back(op);
+    return out;
+  };
+
+  nmeta_ = static_cast<int>(plan_.steps.size());
+  for (std::size_t si = 0; si < plan_.steps.size(); ++si) {
+    const auto& step = plan_.steps[si];
+    auto li = live.find(step.lhs), ri = live.find(step.rhs);
+    if (li == live.end() || ri == live.end())
+      throw std::invalid_argument("execute: missing operand " + step.lhs + " or " + step.rhs);
+    View L = li->second, R = ri->second;
+    live.erase(li);
+    live.erase(step.rhs);
+
+    std::vector<Label> con_l, con_r, lfree, rfree;
+    for (const auto& l : L.labels) (R.has(l) ? con_l : lfree).push_back(l);
+    for (const auto& l : R.labels) (L.has(l) ? con_r : rfree).push_back(l);
+    std::int64_t m = 1, nn = 1, k = 1;
+    for (const auto& l : lfree) m *= L.dim_of(l);
+    for (const auto& l : rfree) nn *= R.dim_of(l);
+    for (const auto& l : con_l) {
+      if (L.dim_of(l) != R.dim_of(l)) throw std::invalid_argument("contract: extent mismatch on " + l);
+      k *= L.dim_of(l);
+    }
+    constexpr std::int64_t kMaxVolume = std::int64_t{1} << 33;  // contraction.hpp:95, :189-191
+    if (m * k > kMaxVolume || k * nn > kMaxVolume || m * nn > kMaxVolume)
+      throw std::length_error("contract_ttgt: volume overflow");
+
+    // Layout choice: contracted order taken from L or from R; an operand is
+    // used in place when dense with the contracted labels as a suffix/prefix.
+    struct Choice {
+      std::vector<Label> con;
+      bool use_a = false, ta = false, use_b = false, tb = false;
+      std::int64_t cost = 0;
+    };
+    auto evaluate = [&](const std::vector<Label>& con) {
+      Choice ch;
+      ch.con = con;
+      const std::size_t nc = con.size();
+      if (L.dense()) {
+        if (seq_equal(L.labels, L.labels.size() - nc, con)) { ch.use_a = true; ch.ta = false; }
+        else if (seq_equal(L.labels, 0, con)) { ch.use_a = true; ch.ta = true; }
+      }
+      if (R.dense()) {
+        if (seq_equal(R.labels, 0, con)) { ch.use_b = true; ch.tb = false; }
+        else if (seq_equal(R.labels, R.labels.size() - nc, con)) { ch.use_b = true; ch.tb = true; }
+      }
+      ch.cost = (ch.use_a ? 0 : L.volume()) + (ch.use_b ? 0 : R.volume());
+      return ch;
+    };
+    Choice best = evaluate(con_l);
+    Choice alt = evaluate(con_r);
+    if (alt.cost < best.cost) best = alt;
+
+    const int op_first = static_cast<int>(ops_.size());
+    View A = L, B = R;
+    if (!best.use_a) {
+      std::vector<Label> order = lfree;
+      order.insert(order.end(), best.con.begin(), best.con.end());
+      A = permute_to(L, order, static_cast<int>(si));
+      best.ta = false;
+    }
+    if (!best.use_b) {
+      std::vector<Label> order = best.con;
+      order.insert(order.end(), rfree.begin(), rfree.end());
+      B = permute_to(R, order, static_cast<int>(si));
+      best.tb = false;
+    }
+    // Free-label orders as laid out in the operands.
+    std::vector<Label> a_free, b_free;
+    for (const auto& l : A.labels)
+      if (!R.has(l)) a_free.push_back(l);
+    for (const auto& l : B.labels)
+      if (!L.has(l)) b_free.push_back(l);
+
+    Op g;
+    g.kind = 1;
+    g.step = static_cast<int>(si);
+    g.a = as_operand(A);
+    g.b = as_operand(B);
+    g.m = m;
+    g.n = nn;
+    g.k = k;
+    g.ta = best.ta;
+    g.tb = best.tb;
+    g.meta_a = A.meta;
+    g.meta_b = B.meta;
+    g.meta_c = static_cast<int>(si);
+    g.flops = step.flops;
+    g.tc = opt_.tensor_cores && dev::cgemm_tc_eligible(m, nn, k, g.ta, g.tb);
+    g.ws_bytes = g.tc ? dev::cgemm_tc_workspace_bytes(m, nn, k, g.ta, g.tb) : dev::cgemm_workspace_bytes(m, nn, k);
+    touch(A.buf);
+    touch(B.buf);
+    g.c = new_buf(m * nn * 8);
+    if (g.ws_bytes > 0) g.ws = new_buf(g.ws_bytes);
+    ops_.push_back(g);
+    (void)op_first;
+
+    View C;
+    C.buf = g.c;
+    C.off = 0;
+    C.meta = static_cast<int>(si);
+    C.labels = a_free;
+    C.labels.insert(C.labels.end(), b_free.begin(), b_free.end());
+    for (const auto& l : C.labels) C.dims.push_back(A.has(l) ? A.dim_of(l) : B.dim_of(l));
+    C.strides = row_major_strides(C.dims);
+    live[step.out] = std::move(C);
+  }
+
+  if (live.size() != 1) throw std::invalid_argument("execute: plan left multiple tensors");
+  View F = live.begin()->second;
+  std::vector<Label> want;
+  for (int q : plan_.open_qubits) want.push_back(open_label(q));
+  std::sort(want.begin(), want.end());
+  {
+    std::vector<Label> have = F.labels;
+    std::sort(have.begin(), have.end());
+    if (have != want) throw std::invalid_argument("execute: final tensor does not match the open qubits");
+  }
+  if (F.labels != want || !F.dense()) F = permute_to(F, want, -1);
+  Op acc;
+  acc.kind = 2;
+  acc.src = as_operand(F);
+  acc.meta_c = F.meta;
+  acc.count = F.volume();
+  touch(F.buf);
+  ops_.push_back(acc);
+  if (F.meta < 0) {
+    // Single-node network: no step produced a meta; use a zeroed slot.
+    ops_.back().meta_c = nmeta_;
+    ++nmeta_;
+  }
+}
+
+void Engine::pack_buffers() {
+  // First-fit over lifetimes, largest buffers first within equal starts.
+  std::vector<int> order(bufs_.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    if (bufs_[static_cast<std::size_t>(x)].first != bufs_[static_cast<std::size_t>(y)].first)
+      return bufs_[static_cast<std::size_t>(x)].first < bufs_[static_cast<std::size_t>(y)].first;
+    return bufs_[static_cast<std::size_t>(x)].bytes > bufs_[static_cast<std::size_t>(y)].bytes;
+  });
+  std::vector<int> placed;
+  arena_bytes_ = 0;
+  for (int id : order) {
+    Buffer& b = bufs_[static_cast<std::size_t>(id)];
+    std::vector<std::pair<std::int64_t, std::int64_t>> busy;
+    for (int p : placed) {
+      const Buffer& o = bufs_[static_cast<std::size_t>(p)];
+      if (o.first <= b.last && b.first <= o.last) busy.emplace_back(o.offset, o.offset + o.bytes);
+    }
+    std::sort(busy.begin(), busy.end());
+    std::int64_t off = 0;
+    for (const auto& [lo, hi] : busy) {
+      if (off + b.bytes <= lo) break;
+      off = std::max(off, hi);
+    }
+    b.offset = off;
+    arena_bytes_ = std::max(arena_bytes_, off + b.bytes);
+    placed.push_back(id);
+  }
+}
+
+void* Engine::ptr(const Operand& o, const std::vector<std::int64_t>& node_off) const {
+  std::int64_t e = o.off;
+  if (o.node >= 0) e += node_off[static_cast<std::size_t>(o.node)];
+  return arena_ + bufs_[static_cast<std::size_t>(o.buf)].offset + e * 8;
+}
+
+std::int64_t Engine::prepare(const std::vector<int>& x1_bits) {
+  if (static_cast<int>(x1_bits.size()) != circuit_.num_qubits())
+    throw std::invalid_argument("fold: bitstring length != qubit count");
+  std::vector<int> open;
+  for (std::size_t q = 0; q < x1_bits.size(); ++q)
+    if (x1_bits[q] < 0) open.push_back(static_cast<int>(q));
+  if (open != plan_.open_qubits) throw std::invalid_argument("x1 open qubits do not match the plan's open qubits");
+  GridNetwork net = fold_worldlines(circuit_, x1_bits);
+  std::vector<std::vector<cfloat>> data;
+  data.reserve(net.nodes.size());
+  for (auto& t : net.nodes) data.push_back(std::move(t.data));
+  return prepare_nodes(data);
+}
+
+std::int64_t Engine::prepare_nodes(const std::vector<std::vector<cfloat>>& data) {
+  if (data.size() != node_vol_.size()) throw std::invalid_argument("prepare_nodes: node count mismatch");
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  // The staging buffer may still feed an in-flight copy.
+  check(cudaStreamSynchronize(stream_), "staging sync");
+  for (std::size_t q = 0; q < data.size(); ++q) {
+    if (static_cast<std::int64_t>(data[q].size()) != node_vol_[q])
+      throw std::invalid_argument("prepare_nodes: node volume mismatch");
+    std::memcpy(staging_ + node_elem_off_[q], data[q].data(), data[q].size() * sizeof(cfloat));
+  }
+  check(cudaMemcpyAsync(arena_ + bufs_[0].offset, staging_, static_cast<std::size_t>(node_bytes_),
+                        cudaMemcpyHostToDevice, stream_),
+        "node upload");
+  return node_bytes_;
+}
+
+void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot) {
+  const Op& op = ops_[i];
+  int launches = 0;
+  if (opt_.profile) check(cudaEventRecord(ev_[2 * i], stream_), "event");
+  if (op.kind == 0) {
+    const std::int64_t base = op.src.off + (op.src.node >= 0 ? node_off[static_cast<std::size_t>(op.src.node)] : 0);
+    check(dev::permute(arena_ + bufs_[static_cast<std::size_t>(op.src.buf)].offset, base,
+                       arena_ + bufs_[static_cast<std::size_t>(op.dst)].offset, static_cast<int>(op.ext.size()),
+                       op.ext.data(), op.istr.data(), stream_, &launches),
+          "permute");
+  } else if (op.kind == 1) {
+    dev::GemmArgs g{};
+    g.a = ptr(op.a, node_off);
+    g.b = ptr(op.b, node_off);
+    g.c = arena_ + bufs_[static_cast<std::size_t>(op.c)].offset;
+    g.m = op.m;
+    g.n = op.n;
+    g.k = op.k;
+    g.trans_a = op.ta;
+    g.trans_b = op.tb;
+    g.meta_a = op.meta_a >= 0 ? metas_ + op.meta_a : nullptr;
+    g.meta_b = op.meta_b >= 0 ? metas_ + op.meta_b : nullptr;
+    g.norm_a = op.meta_a >= 0;
+    g.norm_b = op.meta_b >= 0;
+    g.meta_c = metas_ + op.meta_c;
+    g.workspace = op.ws >= 0 ? arena_ + bufs_[static_cast<std::size_t>(op.ws)].offset : nullptr;
+    g.workspace_bytes = op.ws_bytes;
+    if (op.tc) check(dev::cgemm_tc(g, stream_, &launches), "cgemm_tc");
+    else check(dev::cgemm(g, stream_, &launches), "cgemm");
+  } else {
+    check(dev::accumulate(ptr(op.src, node_off), metas_ + op.meta_c, op.count, acc_, per_slice_slot, stream_, &launches),
+          "accumulate");
+  }
+  if (opt_.profile) check(cudaEventRecord(ev_[2 * i + 1], stream_), "event");
+  launches_ += launches;
+}
+
+void Engine::run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) {
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  if (reset) check(cudaMemsetAsync(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_), stream_), "acc reset");
+  if (per_slice) {
+    const std::int64_t need = static_cast<std::int64_t>(slice_ids.size()) * batch_;
+    if (need > per_slice_cap_) {
+      check(cudaStreamSynchronize(stream_), "sync");
+      if (per_slice_) cudaFree(per_slice_);
+      check(cudaMalloc(&per_slice_, sizeof(double2) * static_cast<std::size_t>(need)), "per-slice cudaMalloc");
+      per_slice_cap_ = need;
+    }
+    per_slice_used_ = static_cast<std::int64_t>(slice_ids.size());
+  } else {
+    per_slice_used_ = 0;
+  }
+  if (events_pending_) profile();  // fold finished timings before reusing events
+  for (std::size_t s = 0; s < slice_ids.size(); ++s) {
+    const auto digits = cut_digits(shape_, plan_.cut, slice_ids[s]);
+    std::vector<std::int64_t> node_off(node_vol_.size(), 0);
+    for (std::size_t q = 0; q < node_vol_.size(); ++q)
+      for (std::size_t ci = 0; ci < node_cut_axes_[q].size(); ++ci) {
+        const int ax = node_cut_axes_[q][ci];
+        if (ax >= 0) node_off[q] += digits[ci] * node_full_strides_[q][static_cast<std::size_t>(ax)];
+      }
+    check(cudaMemsetAsync(metas_, 0, sizeof(dev::TMeta) * static_cast<std::size_t>(nmeta_), stream_), "meta reset");
+    void* slot = per_slice ? static_cast<void*>(per_slice_ + static_cast<std::int64_t>(s) * batch_) : nullptr;
+    for (std::size_t i = 0; i < ops_.size(); ++i) {
+      launch_op(i, node_off, slot);
+    }
+    if (opt_.profile) {
+      // Events are reused per slice: harvest this slice's timings.
+      check(cudaStreamSynchronize(stream_), "profile sync");
+      for (std::size_t i = 0; i < ops_.size(); ++i) {
+        float ms = 0.f;
+        check(cudaEventElapsedTime(&ms, ev_[2 * i], ev_[2 * i + 1]), "elapsed");
+        op_ms_[i] += ms;
+        op_execs_[i] += 1;
+      }
+    }
+  }
+}
+
+void Engine::results(std::vector<cdouble>* amps, std::vector<cdouble>* per_slice) {
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  if (amps) {
+    amps->resize(static_cast<std::size_t>(batch_));
+    check(cudaMemcpyAsync(amps->data(), acc_, sizeof(double2) * static_cast<std::size_t>(batch_), cudaMemcpyDeviceToHost,
+                          stream_),
+          "result copy");
+  }
+  if (per_slice) {
+    per_slice->resize(static_cast<std::size_t>(per_slice_used_ * batch_));
+    if (per_slice_used_ > 0)
+      check(cudaMemcpyAsync(per_slice->data(), per_slice_, sizeof(double2) * per_slice->size(), cudaMemcpyDeviceToHost,
+                            stream_),
+            "per-slice copy");
+  }
+  check(cudaStreamSynchronize(stream_), "result sync");
+}
+
+void Engine::synchronize() {
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  check(cudaStreamSynchronize(stream_), "sync");
+}
+
+std::vector<OpProfile> Engine::profile() {
+  synchronize();
+  events_pending_ = false;
+  std::vector<OpProfile> out;
+  for (std::size_t i = 0; i < ops_.size(); ++i) {
+    const Op& op = ops_[i];
+    OpProfile p{};
+    p.kind = op.kind;
+    p.step = op.step;
+    p.m = op.kind == 1 ? op.m : op.count;
+    p.n = op.kind == 1 ? op.n : 0;
+    p.k = op.kind == 1 ? op.k : 0;
+    p.flops = op.kind == 1 ? op.flops : 0;
+    p.bytes = op.kind == 0 ? 16 * op.count : op.kind == 1 ? 8 * (op.m * op.k + op.k * op.n + op.m * op.n) : 24 * op.count;
+    p.ms_total = op_ms_[i];
+    p.executions = op_execs_[i];
+    p.tc = op.tc ? 1 : 0;
+    out.push_back(p);
+  }
+  return out;
+}
+
+void Engine::reset_profile() {
+  std::fill(op_ms_.begin(), op_ms_.end(), 0.0);
+  std::fill(op_execs_.begin(), op_execs_.end(), 0);
+}
+
+std::string Engine::describe() const {
+  std::ostringstream os;
+  os << "arena " << arena_bytes_ << " B, nodes " << node_bytes_ << " B, ops " << ops_.size() << "\n";
+  for (const auto& op : ops_) {
+    if (op.kind == 0) os << "  permute step " << op.step << " elems " << op.count << " rank " << op.ext.size() << "\n";
+    else if (op.kind == 1)
+      os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << (op.ta ? " TA" : "")
+         << (op.tb ? " TB" : "") << (op.tc ? " tc" : "") << "\n";
+    else os << "  accumulate " << op.count << "\n";
+  }
+  return os.str();
+}
+
+std::vector<std::pair<std::string, cdouble>> amplitude_batch(Engine& e, const std::vector<int>& x1_bits,
+                                                             const std::vector<std::int64_t>& slice_ids) {
+  e.prepare(x1_bits);
+  e.run(slice_ids, /*reset=*/true, /*per_slice=*/false);
+  std::vector<cdouble> amps;
+  e.results(&amps, nullptr);
+  std::vector<std::pair<std::string, cdouble>> out;
+  out.reserve(amps.size());
+  for (std::size_t j = 0; j < amps.size(); ++j) out.emplace_back(merge_bits(x1_bits, e.plan().open_qubits, j), amps[j]);
+  return out;
+}
+
+AmplitudeOutput run_amplitudes(Engine& e, const std::vector<std::string>& bitstrings, Fraction f, std::uint64_t seed) {
+  const int n = e.circuit().num_qubits();
+  if (!e.plan().open_qubits.empty()) throw std::invalid_argument("run_amplitudes: plan must close every output");
+  for (const auto& b : bitstrings)
+    if (static_cast<int>(b.size()) != n) throw std::invalid_argument("bitstring length != qubit count: " + b);
+  AmplitudeOutput out;
+  out.slice_ids = select_slices(f, e.plan().num_slices, seed);
+  for (const auto& b : bitstrings) {
+    std::vector<int> bits(static_cast<std::size_t>(n));
+    for (int q = 0; q < n; ++q) {
+      if (b[static_cast<std::size_t>(q)] != '0' && b[static_cast<std::size_t>(q)] != '1')
+        throw std::invalid_argument("bitstring: bad character");
+      bits[static_cast<std::size_t>(q)] = b[static_cast<std::size_t>(q)] - '0';
+    }
+    e.prepare(bits);
+    e.run(out.slice_ids, true, false);
+    std::vector<cdouble> amps;
+    e.results(&amps, nullptr);
+    out.amplitudes.emplace_back(b, amps[0]);
+    out.total_flops += e.plan().flops_per_slice * out.slice_ids.size();
+  }
+  return out;
+}
+
+}  // namespace qsg

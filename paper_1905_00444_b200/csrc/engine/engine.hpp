@@ -1,0 +1,170 @@
+// Device executor for the sliced contraction (replaces execute_slice,
+// proj/src/engine.cpp:182-245, and the slice loops of batch_amplitudes,
+// src/sampler.cpp:17-36, and run_amplitudes, src/engine.cpp:300-378).
+//
+// A plan is compiled ONCE into a static device program:
+//   * node tensors live in one region of a single HBM arena (uploaded per
+//     x1 batch from pinned staging); a cut is a per-slice base offset plus
+//     dropped strides, so apply_cut costs nothing;
+//   * each plan step becomes [K1 permute of an operand when its layout is
+//     unusable] + one K2 CGEMM writing C = [lfree, rfree].  The executor
+//     picks the contracted-label order and N/T operand layouts that avoid
+//     permutes, and never permutes outputs back to sorted order (only the
+//     final tensor is put in sorted open-label order, the one layout the
+//     reference exposes, src/sampler.cpp:38-40);
+//   * intermediates, permute scratch and split-K workspaces get static
+//     arena offsets from a liveness-based first-fit packing, so a slice
+//     does no allocation and every slice reuses the same layout;
+//   * renormalisation state (TMeta) is device resident; nothing
+//     synchronises with the host inside a slice.
+// Slices run back to back on one stream; K3 accumulates them in order.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../device/kernels.hpp"
+#include "../host/qsg_host.hpp"
+
+namespace qsg {
+
+struct EngineOptions {
+  int device = 0;
+  bool profile = false;     // CUDA events around every kernel op
+  bool tensor_cores = true; // allow the tcgen05 GEMM for eligible steps
+};
+
+struct OpProfile {
+  int kind;          // 0 permute, 1 gemm, 2 accumulate/final
+  int step;          // plan step index (-1 for the final op)
+  std::int64_t m, n, k;      // gemm shape (permute: elements in m)
+  std::uint64_t flops;       // Eq.(1) flops of the step (gemm ops)
+  std::int64_t bytes;        // algorithmic bytes moved (permute: 16 B/elem)
+  double ms_total;           // summed over executions
+  std::int64_t executions;
+  int tc;                    // 1 if the tcgen05 kernel ran
+};
+
+class Engine {
+ public:
+  Engine(const Circuit& c, const ContractionPlan& plan, const EngineOptions& opt);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const Circuit& circuit() const { return circuit_; }
+  const ContractionPlan& plan() const { return plan_; }
+  std::int64_t batch_size() const { return batch_; }
+  std::int64_t arena_bytes() const { return arena_bytes_; }
+  std::int64_t node_bytes() const { return node_bytes_; }
+  cudaStream_t stream() const { return stream_; }
+  int device() const { return opt_.device; }
+
+  // Folds the circuit for x1 (one entry per qubit, -1 exactly on the plan's
+  // open qubits) on the host and uploads the node tensors (async H2D from
+  // pinned staging).  Returns the H2D byte count.
+  std::int64_t prepare(const std::vector<int>& x1_bits);
+  // Uploads pre-folded node tensors given in fold layout (tests / device
+  // fold).  data[q] has the node's full (uncut) volume.
+  std::int64_t prepare_nodes(const std::vector<std::vector<cfloat>>& data);
+
+  // Runs the slices in the given order on the engine stream (async).
+  // reset: zero the batch accumulator first.  per_slice: keep every
+  // slice's contribution (slot i for slice_ids[i]).
+  void run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice);
+
+  // Copies results to the host (synchronises the stream).
+  void results(std::vector<cdouble>* amps, std::vector<cdouble>* per_slice);
+  void synchronize();
+
+  std::int64_t launches() const { return launches_; }
+  std::vector<OpProfile> profile();  // synchronises
+  void reset_profile();
+  void set_profile(bool on);
+  std::string describe() const;      // human-readable program listing
+
+ private:
+  struct Buffer {
+    std::int64_t bytes = 0;
+    int first = 0, last = 0;
+    std::int64_t offset = 0;
+  };
+  struct Operand {
+    int buf = -1;
+    std::int64_t off = 0;   // elements, static part
+    int node = -1;          // node whose per-slice cut offset applies
+  };
+  struct Op {
+    int kind = 0;  // 0 permute, 1 gemm, 2 final accumulate
+    int step = -1;
+    Operand src;   // permute source / accumulate source
+    std::vector<std::int64_t> ext, istr;
+    int dst = -1;  // permute destination buffer
+    Operand a, b;  // gemm
+    int c = -1;
+    std::int64_t m = 0, n = 0, k = 0;
+    bool ta = false, tb = false;
+    int meta_a = -1, meta_b = -1, meta_c = -1;
+    int ws = -1;
+    std::int64_t ws_bytes = 0;
+    bool tc = false;
+    std::int64_t count = 0;  // accumulate / permute elements
+    std::uint64_t flops = 0;
+  };
+
+  void compile();
+  void pack_buffers();
+  void* ptr(const Operand& o, const std::vector<std::int64_t>& node_off) const;
+  void launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot);
+
+  Circuit circuit_;
+  ContractionPlan plan_;
+  NetworkShape shape_;       // fold layout (open label at axis 0)
+  EngineOptions opt_;
+  cudaStream_t stream_ = nullptr;
+  std::int64_t batch_ = 1;
+
+  // Node layout (full, uncut) inside the node region.
+  std::vector<std::int64_t> node_elem_off_, node_vol_;
+  std::vector<std::vector<std::int64_t>> node_full_strides_;
+  std::vector<std::vector<int>> node_cut_axes_;  // per node: fixed cut index -> axis
+  std::vector<std::pair<int, std::int64_t>> cut_terms_;  // unused placeholder
+  std::int64_t node_bytes_ = 0;
+
+  std::vector<Buffer> bufs_;
+  std::vector<Op> ops_;
+  std::int64_t arena_bytes_ = 0;
+  char* arena_ = nullptr;
+  dev::TMeta* metas_ = nullptr;
+  int nmeta_ = 0;
+  double2* acc_ = nullptr;
+  double2* per_slice_ = nullptr;
+  std::int64_t per_slice_cap_ = 0;
+  std::int64_t per_slice_used_ = 0;
+  cfloat* staging_ = nullptr;
+  std::int64_t launches_ = 0;
+
+  std::vector<cudaEvent_t> ev_;
+  std::vector<double> op_ms_;
+  std::vector<std::int64_t> op_execs_;
+  bool events_pending_ = false;
+};
+
+// Reference-named drivers on top of the engine.
+// amplitude_batch (src/sampler.cpp:111-120): (bitstring, amplitude) pairs.
+std::vector<std::pair<std::string, cdouble>> amplitude_batch(Engine& e, const std::vector<int>& x1_bits,
+                                                             const std::vector<std::int64_t>& slice_ids);
+
+struct AmplitudeOutput {
+  std::vector<std::pair<std::string, cdouble>> amplitudes;
+  std::vector<std::int64_t> slice_ids;
+  std::uint64_t total_flops = 0;
+};
+// run_amplitudes (src/engine.cpp:300-378) for closed plans.
+AmplitudeOutput run_amplitudes(Engine& e, const std::vector<std::string>& bitstrings, Fraction f, std::uint64_t seed);
+
+}  // namespace qsg
