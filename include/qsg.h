@@ -103,6 +103,13 @@ int qsg_permute_dev(const void* in_dev, int64_t base, void* out_dev, int rank, c
 int qsg_cgemm_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_a,
                   int trans_b, void* stream);
 
+/* K2 on the tcgen05 tensor cores (3xTF32, FP32-level accuracy).  Requires
+ * m % 128 == 0, n % 64 == 0, k % 16 == 0, A row-major; returns
+ * QSG_ERR_INVALID_ARGUMENT otherwise.  Allocates its B-expansion workspace
+ * (32*n*k bytes) internally and synchronises the stream. */
+int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_b,
+                     void* stream);
+
 /* ---------------------------------------------------------------------------
  * Tensor operations on host buffers, computed on the GPU (synchronous)
  * ------------------------------------------------------------------------- */

@@ -100,6 +100,7 @@ def lib():
         "qsg_draw_x1": (i32, [i32, P(i32), i32, u64, u64, P(i32)]),
         "qsg_permute_dev": (i32, [vp, i64, vp, i32, P(i64), P(i64), vp]),
         "qsg_cgemm_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, vp]),
+        "qsg_cgemm_tc_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, vp]),
         "qsg_transpose": (i32, [i32, P(i64), fp, P(i32), fp]),
         "qsg_contract": (i32, [i32, P(i32), P(i64), fp, C.c_double, i32, P(i32), P(i64), fp, C.c_double, i32, P(i32),
                                fp, dp, P(u64), i32]),

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "device/kernels.hpp"
+#include "device/kernels_tc.hpp"
 #include "engine/engine.hpp"
 #include "host/qsg_host.hpp"
 
@@ -248,6 +249,29 @@ int qsg_cgemm_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, 
     g.trans_a = trans_a != 0;
     g.trans_b = trans_b != 0;
     cuda_check(qsg::dev::cgemm(g, static_cast<cudaStream_t>(stream)), "cgemm");
+  });
+}
+
+int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_b,
+                     void* stream) {
+  return guarded([&] {
+    if (!qsg::dev::cgemm_tc_eligible(m, n, k, false, trans_b != 0))
+      throw std::invalid_argument("cgemm_tc: shape not eligible for the tensor-core path");
+    const std::int64_t ws = qsg::dev::cgemm_tc_workspace_bytes(m, n, k, false, trans_b != 0);
+    DevBuf w(static_cast<std::size_t>(ws));
+    qsg::dev::GemmArgs g{};
+    g.a = a_dev;
+    g.b = b_dev;
+    g.c = c_dev;
+    g.m = m;
+    g.n = n;
+    g.k = k;
+    g.trans_b = trans_b != 0;
+    g.workspace = w.p;
+    g.workspace_bytes = ws;
+    auto s = static_cast<cudaStream_t>(stream);
+    cuda_check(qsg::dev::cgemm_tc(g, s), "cgemm_tc");
+    cuda_check(cudaStreamSynchronize(s), "cgemm_tc sync");
   });
 }
 

@@ -1,24 +1,455 @@
-// K2 tensor-core path (tcgen05 kind::tf32, 3xTF32 split) -- under
-// construction; until validated on hardware every shape routes to the
-// general FP32 kernel (cgemm.cu).
+// K2 tensor-core path: the contraction GEMM of contract_ttgt
+// (include/qsim/contraction.hpp:208-214) on the 5th-generation tensor cores.
+//
+// Complex -> real embedding.  A complex row-major A[m][k] IS a real matrix
+// A_r[m][2k] (re/im interleaved along K), and with
+//   B_r^T[2j  ][2p..2p+1] = ( Re b_pj, -Im b_pj )
+//   B_r^T[2j+1][2p..2p+1] = ( Im b_pj,  Re b_pj )
+// the real product C_r[m][2n] = A_r * B_r is exactly the complex row-major
+// C[m][n] (C_r row = re/im interleaved).  So the large operand A and the
+// output C are consumed/produced in place, K-major, with no repacking; only
+// the (small) B operand is expanded once per GEMM by tc_prep_b_kernel.  The
+// real GEMM does 4 real MACs per complex MAC = the 8 flops of Eq.(1).
+//
+// FP32 accuracy from TF32 tensor cores (3xTF32): x = hi + lo with
+// hi = rna_tf32(x), lo = x - hi (exact), and
+//   A*B ~= A_hi*B_hi + A_hi*B_lo + A_lo*B_hi      (FP32 accumulate in TMEM),
+// leaving only the lo*lo term (~2^-22 relative).  B is split in the prep
+// kernel; A is split in shared memory by converter warps as each stage
+// lands (no extra HBM traffic or footprint for the big operand).
+//
+// Kernel anatomy (one CTA per 128 x BN output tile, 6 warps):
+//   warp 0     TMA producer: A tile [128 x 32 fp32] and B_hi/B_lo tiles
+//              [BN x 32] per stage, SWIZZLE_128B, mbarrier complete_tx;
+//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
+//              (kind::tf32, M=128, N=BN, K=8), tcgen05.commit -> barriers;
+//   warps 2-5  converters (A -> A_hi in place, A_lo alongside, then
+//              fence.proxy.async) and, after the mainloop, the epilogue:
+//              tcgen05.ld accumulator rows, apply the operands' pending
+//              power-of-two renormalisation, max|c|^2 -> TMeta, store C.
+#include <cuda.h>
+
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <stdexcept>
+#include <string>
 
 #include "kernels_tc.hpp"
 
 namespace qsg::dev {
+
+__device__ __forceinline__ int tc_pending_shift(const TMeta* m, bool norm) {
+  if (!norm || m == nullptr) return 0;
+  const unsigned bits = m->maxsq_bits;
+  if (bits == 0) return 0;
+  const double mx = sqrt(static_cast<double>(__uint_as_float(bits)));
+  int e = 0;
+  const double fr = frexp(mx, &e);
+  return fr == 0.5 ? e - 1 : e;
+}
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements of K_real per stage (= one 128-byte swizzle row)
+constexpr int kThreads = 192;
+constexpr int A_BYTES = BM * BK * 4;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = BN >= 256 ? 2 : 3;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int TMEM_COLS = BN;  // power of two >= 32
+};
+
+struct TcParams {
+  float* c;  // complex64 C[m][n] as fp32 [m][2n]
+  long long m, n2;  // rows, real columns (2n)
+  int kblocks;
+  int n_tiles;  // output tiles along N; blockIdx.x = m_tile * n_tiles + n_tile
+  const TMeta* meta_a;
+  const TMeta* meta_b;
+  TMeta* meta_c;
+  int norm_a, norm_b;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms
+// of 1024 B; SBO = 1024 B; version 1; layout type 2 = SWIZZLE_128B).
+__device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;              // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;      // SBO
+  d |= static_cast<uint64_t>(1) << 46;              // version (Blackwell)
+  d |= static_cast<uint64_t>(2) << 61;              // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M=128, N=BN.
+template <int BN>
+__host__ __device__ constexpr uint32_t tf32_idesc() {
+  return (1u << 4)               // D format F32
+         | (2u << 7)             // A format TF32
+         | (2u << 10)            // B format TF32
+         | (0u << 15) | (0u << 16)  // K-major A and B
+         | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return __uint_as_float(u);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    cgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
+                    const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
+  using Cfg = TcCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* conv = full + Cfg::STAGES;
+  uint64_t* empty = conv + Cfg::STAGES;
+  uint64_t* tmem_full = empty + Cfg::STAGES;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n_tile = static_cast<int>(blockIdx.x % p.n_tiles);
+  const long long m_tile = blockIdx.x / p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_bhi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_blo) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "n"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_slot;
+  const int kblocks = p.kblocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        const uint32_t ph = (kb / Cfg::STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+        mbar_expect_tx(&full[s], A_BYTES + 2 * Cfg::B_BYTES);
+        tma_load_2d(&map_a, &full[s], st, kb * BK, static_cast<int>(m_tile * BM));
+        tma_load_2d(&map_bhi, &full[s], st + 2 * A_BYTES, kb * BK, n_tile * BN);
+        tma_load_2d(&map_blo, &full[s], st + 2 * A_BYTES + Cfg::B_BYTES, kb * BK, n_tile * BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc<BN>();
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        const uint32_t ph = (kb / Cfg::STAGES) & 1;
+        mbar_wait(&conv[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+        const uint64_t a_hi = kmajor_sw128_desc(smem_u32(st));
+        const uint64_t a_lo = kmajor_sw128_desc(smem_u32(st + A_BYTES));
+        const uint64_t b_hi = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES));
+        const uint64_t b_lo = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES + Cfg::B_BYTES));
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);  // 8 tf32 = 32 bytes along the swizzled row
+          umma_tf32(tmem, a_hi + adv, b_hi + adv, idesc, (kb | kk) != 0 ? 1u : 0u);
+          umma_tf32(tmem, a_hi + adv, b_lo + adv, idesc, 1u);
+          umma_tf32(tmem, a_lo + adv, b_hi + adv, idesc, 1u);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+    __syncwarp();
+  } else {
+    // ---- converters: A -> (A_hi in place, A_lo) per stage ----
+    const int t = threadIdx.x - 64;  // 0..127
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % Cfg::STAGES;
+      const uint32_t ph = (kb / Cfg::STAGES) & 1;
+      mbar_wait(&full[s], ph);
+      float4* a = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES);
+      float4* alo = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES + A_BYTES);
+#pragma unroll
+      for (int i = 0; i < A_BYTES / 16 / 128; ++i) {
+        const int idx = i * 128 + t;
+        const float4 x = a[idx];
+        float4 h, l;
+        h.x = tf32_rna(x.x); l.x = x.x - h.x;
+        h.y = tf32_rna(x.y); l.y = x.y - h.y;
+        h.z = tf32_rna(x.z); l.z = x.z - h.z;
+        h.w = tf32_rna(x.w); l.w = x.w - h.w;
+        a[idx] = h;
+        alo[idx] = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&conv[s]);
+    }
+    // ---- epilogue ----
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    const long long gm = m_tile * BM + row;
+    const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
+    const int shift = sa + sb;
+    float local = 0.f;
+    float* crow = p.c + gm * p.n2 + static_cast<long long>(n_tile) * BN;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = scalbnf(v[i], -shift);
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) local = fmaxf(local, v[i] * v[i] + v[i + 1] * v[i + 1]);
+      float4* dst = reinterpret_cast<float4*>(crow + c0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+    if (p.meta_c) {
+      for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+      if (lane == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
+      if (blockIdx.x == 0 && threadIdx.x == 64)
+        p.meta_c->log_scale = (p.meta_a ? p.meta_a->log_scale : 0.0) + (p.meta_b ? p.meta_b->log_scale : 0.0) + shift;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
+  }
+}
+
+// B (complex, [k][n] or [n][k]) -> B_r^T hi/lo planes [2n][2k] fp32.
+__global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict__ b, float* __restrict__ hi,
+                                                        float* __restrict__ lo, long long n, long long k, int tb) {
+  __shared__ float2 tile[32][33];  // [p_local][j_local]
+  const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    if (!tb) {  // B[p][j], j contiguous
+      const long long p = p0 + r, j = j0 + tx;
+      tile[r][tx] = (p < k && j < n) ? b[p * n + j] : make_float2(0.f, 0.f);
+    } else {    // B[j][p], p contiguous
+      const long long j = j0 + r, p = p0 + tx;
+      tile[tx][r] = (p < k && j < n) ? b[j * k + p] : make_float2(0.f, 0.f);
+    }
+  }
+  __syncthreads();
+  const long long k2 = 2 * k;
+  for (int r = ty; r < 32; r += 8) {
+    const long long j = j0 + r, p = p0 + tx;
+    if (j >= n || p >= k) continue;
+    const float2 v = tile[tx][r];
+    const float re = v.x, im = v.y;
+    float h0, h1, h2, h3;
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(re)); h0 = __uint_as_float(u);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(-im)); h1 = __uint_as_float(u);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(im)); h2 = __uint_as_float(u);
+    h3 = h0;
+    const long long row0 = (2 * j) * k2 + 2 * p, row1 = (2 * j + 1) * k2 + 2 * p;
+    *reinterpret_cast<float2*>(hi + row0) = make_float2(h0, h1);
+    *reinterpret_cast<float2*>(hi + row1) = make_float2(h2, h3);
+    *reinterpret_cast<float2*>(lo + row0) = make_float2(re - h0, -im - h1);
+    *reinterpret_cast<float2*>(lo + row1) = make_float2(im - h2, re - h3);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeFn>(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  if (!fn) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled lookup: entry point unavailable");
+  return fn;
+}
+
+// 2-D fp32 K-major map: inner dim `cols` (contiguous), outer `rows`; box
+// [box_rows x 32] with 128-byte swizzle.
+CUtensorMap make_map(const void* base, long long cols, long long rows, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
+  return m;
+}
+
+int tc_bn(std::int64_t n) {
+  const char* env = std::getenv("QSG_TC_BN");
+  const int want = env ? std::atoi(env) : 256;
+  if (want == 256 && (2 * n) % 256 == 0) return 256;
+  return 128;
+}
+
+template <int BN>
+void setup_attr() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(cgemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TcCfg<BN>::SMEM);
+  });
+}
+
+}  // namespace
 
 bool tc_enabled() {
   const char* env = std::getenv("QSG_TENSOR_CORES");
   return !(env && env[0] == '0');
 }
 
-bool cgemm_tc_eligible(std::int64_t, std::int64_t, std::int64_t, bool, bool) { return false; }
+bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool /*trans_b*/) {
+  if (!tc_enabled() || trans_a) return false;
+  if (m % BM != 0 || (2 * n) % 128 != 0 || (2 * k) % BK != 0) return false;
+  // Worth it only for real work: >= ~1 GFLOP and a non-trivial K.
+  return 8.0 * static_cast<double>(m) * n * k >= 1e9 && k >= 64;
+}
 
-std::int64_t cgemm_tc_workspace_bytes(std::int64_t, std::int64_t, std::int64_t, bool, bool) { return 0; }
+std::int64_t cgemm_tc_workspace_bytes(std::int64_t /*m*/, std::int64_t n, std::int64_t k, bool, bool) {
+  return 2 * (2 * n) * (2 * k) * 4;  // B_r^T hi + lo
+}
 
-cudaError_t cgemm_tc(const GemmArgs&, cudaStream_t, int*) {
-  throw std::runtime_error("cgemm_tc: tensor-core path not available");
+cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
+  if (!cgemm_tc_eligible(g.m, g.n, g.k, g.trans_a, g.trans_b)) throw std::invalid_argument("cgemm_tc: shape not eligible");
+  if (g.workspace == nullptr || g.workspace_bytes < cgemm_tc_workspace_bytes(g.m, g.n, g.k, g.trans_a, g.trans_b))
+    throw std::invalid_argument("cgemm_tc: workspace too small");
+  float* bhi = static_cast<float*>(g.workspace);
+  float* blo = bhi + (2 * g.n) * (2 * g.k);
+  {
+    dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
+    tc_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k, g.trans_b ? 1 : 0);
+    if (launches) ++*launches;
+  }
+  const int bn = tc_bn(g.n);
+  const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
+  const CUtensorMap mbh = make_map(bhi, 2 * g.k, 2 * g.n, bn);
+  const CUtensorMap mbl = make_map(blo, 2 * g.k, 2 * g.n, bn);
+  TcParams p{};
+  p.c = static_cast<float*>(g.c);
+  p.m = g.m;
+  p.n2 = 2 * g.n;
+  p.kblocks = static_cast<int>((2 * g.k) / BK);
+  p.meta_a = g.meta_a;
+  p.meta_b = g.meta_b;
+  p.meta_c = g.meta_c;
+  p.norm_a = g.norm_a;
+  p.norm_b = g.norm_b;
+  const long long mt = g.m / BM, nt = (2 * g.n) / bn;
+  if (mt * nt > 2147483647LL || g.m > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
+  p.n_tiles = static_cast<int>(nt);
+  dim3 grid(static_cast<unsigned>(mt * nt));
+  if (bn == 256) {
+    setup_attr<256>();
+    cgemm_tc_kernel<256><<<grid, kThreads, TcCfg<256>::SMEM, stream>>>(ma, mbh, mbl, p);
+  } else {
+    setup_attr<128>();
+    cgemm_tc_kernel<128><<<grid, kThreads, TcCfg<128>::SMEM, stream>>>(ma, mbh, mbl, p);
+  }
+  if (launches) ++*launches;
+  return cudaGetLastError();
 }
 
 }  // namespace qsg::dev

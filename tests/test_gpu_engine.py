@@ -21,7 +21,10 @@ pytestmark = pytest.mark.gpu
 
 
 def rel(a, b):
-    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    nb = np.linalg.norm(b)
+    if nb == 0:
+        return float(np.linalg.norm(a))  # exact zero contribution (e.g. a cut slice that vanishes)
+    return float(np.linalg.norm(a - b) / nb)
 
 
 @pytest.fixture(scope="module")

@@ -133,3 +133,28 @@ def test_cgemm_device_shapes_vs_fp64(gpu, m, n, k, ta, tb):
     got = dC.cpu().to(torch.complex128)
     err = (got - want).abs().norm() / want.abs().norm()
     assert err < 1e-5 * max(1.0, (k / 4096) ** 0.5), float(err)
+
+
+@pytest.mark.parametrize("m,n,k,tb", [(128, 64, 16, 0), (256, 128, 64, 0), (1024, 256, 256, 0), (512, 192, 80, 1),
+                                      (4096, 128, 1024, 0), (1 << 15, 256, 256, 0)])
+def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb):
+    """tcgen05 3xTF32 path: FP32-level accuracy (1e-5 relative Frobenius, the
+    reference's TTGT tolerance, test_tensor.cpp:120-155)."""
+    import torch
+    g = torch.Generator().manual_seed(m + 3 * n + 7 * k)
+    A = torch.complex(torch.rand(m, k, generator=g) - 0.5, torch.rand(m, k, generator=g) - 0.5)
+    B = torch.complex(torch.rand(k, n, generator=g) - 0.5, torch.rand(k, n, generator=g) - 0.5)
+    want = A.to(torch.complex128) @ B.to(torch.complex128)
+    dA = A.cuda()
+    dB = (B.t().contiguous() if tb else B).cuda()
+    dC = torch.zeros(m, n, dtype=torch.complex64, device="cuda")
+    gpu._check(gpu.lib().qsg_cgemm_tc_dev(dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), m, n, k, tb, None))
+    torch.cuda.synchronize()
+    got = dC.cpu().to(torch.complex128)
+    err = float((got - want).abs().norm() / want.abs().norm())
+    assert err < 1e-5, err
+    # and agrees with the FP32 SIMT kernel to the same level
+    dC2 = torch.zeros_like(dC)
+    gpu._check(gpu.lib().qsg_cgemm_dev(dA.data_ptr(), dB.data_ptr(), dC2.data_ptr(), m, n, k, 0, tb, None))
+    torch.cuda.synchronize()
+    assert float((dC2.cpu().to(torch.complex128) - got).abs().norm() / want.abs().norm()) < 1e-5
