@@ -255,7 +255,7 @@ int qsg_cgemm_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, 
 int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_b,
                      void* stream) {
   return guarded([&] {
-    if (!qsg::dev::cgemm_tc_eligible(m, n, k, false, trans_b != 0))
+    if (!qsg::dev::cgemm_tc_supported(m, n, k, false, trans_b != 0))
       throw std::invalid_argument("cgemm_tc: shape not eligible for the tensor-core path");
     const std::int64_t ws = qsg::dev::cgemm_tc_workspace_bytes(m, n, k, false, trans_b != 0);
     DevBuf w(static_cast<std::size_t>(ws));

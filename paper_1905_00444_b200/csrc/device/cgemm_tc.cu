@@ -18,14 +18,22 @@
 // kernel; A is split in shared memory by converter warps as each stage
 // lands (no extra HBM traffic or footprint for the big operand).
 //
-// Kernel anatomy (one CTA per 128 x BN output tile, 6 warps):
+// Accumulation: the tensor core's FP32 accumulator truncates, so its error
+// grows linearly with K (measured 9e-4 at K=65536).  Partial sums are
+// therefore promoted every kChunk k-blocks (32 complex K) from a
+// double-buffered TMEM accumulator into round-to-nearest FP32 registers,
+// overlapping the MMA of the next chunk (cf. DeepSeek-V3's FP8 promotion).
+//
+// Kernel anatomy (one CTA per 128 x BN output tile, 10 warps):
 //   warp 0     TMA producer: A tile [128 x 32 fp32] and B_hi/B_lo tiles
 //              [BN x 32] per stage, SWIZZLE_128B, mbarrier complete_tx;
 //   warp 1     TMEM allocator + single-thread tcgen05.mma issuer
-//              (kind::tf32, M=128, N=BN, K=8), tcgen05.commit -> barriers;
-//   warps 2-5  converters (A -> A_hi in place, A_lo alongside, then
-//              fence.proxy.async) and, after the mainloop, the epilogue:
-//              tcgen05.ld accumulator rows, apply the operands' pending
+//              (kind::tf32, M=128, N=BN, K=8) into TMEM chunk buffer c&1,
+//              tcgen05.commit -> smem-stage and chunk barriers;
+//   warps 2-9  workers: convert A (A -> A_hi in place, A_lo alongside,
+//              fence.proxy.async), drain finished TMEM chunks (tcgen05.ld)
+//              into register accumulators (row = lane quadrant, half the
+//              columns each), and the epilogue: apply the operands' pending
 //              power-of-two renormalisation, max|c|^2 -> TMeta, store C.
 #include <cuda.h>
 
@@ -54,7 +62,13 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 32;  // fp32 elements of K_real per stage (= one 128-byte swizzle row)
-constexpr int kThreads = 192;
+constexpr int kWorkers = 256;            // warps 2..9
+constexpr int kThreads = 64 + kWorkers;   // + producer warp + MMA warp
+// k-blocks (32 real K each) accumulated in TMEM before promotion to
+// registers: the tensor core's FP32 accumulator truncates, so its error
+// grows linearly with the reduction length (measured ~1.4e-8 * k); 32
+// complex K per chunk keeps it at the 3xTF32 floor (~5e-7).
+constexpr int kChunk = 2;
 constexpr int A_BYTES = BM * BK * 4;
 
 template <int BN>
@@ -63,7 +77,7 @@ struct TcCfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = BN >= 256 ? 2 : 3;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr int TMEM_COLS = BN;  // power of two >= 32
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered chunk accumulator (power of two)
 };
 
 struct TcParams {
@@ -153,20 +167,17 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(u);
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 template <int BN>
@@ -174,13 +185,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     cgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
                     const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
   using Cfg = TcCfg<BN>;
+  constexpr int HALF = BN / 2;  // accumulator columns owned by one worker thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* conv = full + Cfg::STAGES;
   uint64_t* empty = conv + Cfg::STAGES;
-  uint64_t* tmem_full = empty + Cfg::STAGES;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + Cfg::STAGES;   // [2] TMEM chunk buffer ready
+  uint64_t* acc_empty = acc_full + 2;          // [2] TMEM chunk buffer drained
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -190,10 +203,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      mbar_init(&conv[s], kWorkers);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kWorkers);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -211,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_slot;
   const int kblocks = p.kblocks;
+  const int nchunks = (kblocks + kChunk - 1) / kChunk;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -228,74 +245,103 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = tf32_idesc<BN>();
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % Cfg::STAGES;
-        const uint32_t ph = (kb / Cfg::STAGES) & 1;
-        mbar_wait(&conv[s], ph);
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
-        const uint64_t a_hi = kmajor_sw128_desc(smem_u32(st));
-        const uint64_t a_lo = kmajor_sw128_desc(smem_u32(st + A_BYTES));
-        const uint64_t b_hi = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES));
-        const uint64_t b_lo = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES + Cfg::B_BYTES));
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * BN);
+        const int kb_end = min(kblocks, (c + 1) * kChunk);
+        for (int kb = c * kChunk; kb < kb_end; ++kb) {
+          const int s = kb % Cfg::STAGES;
+          const uint32_t ph = (kb / Cfg::STAGES) & 1;
+          mbar_wait(&conv[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          const uint64_t a_hi = kmajor_sw128_desc(smem_u32(st));
+          const uint64_t a_lo = kmajor_sw128_desc(smem_u32(st + A_BYTES));
+          const uint64_t b_hi = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES));
+          const uint64_t b_lo = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES + Cfg::B_BYTES));
+          const bool first = kb == c * kChunk;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);  // 8 tf32 = 32 bytes along the swizzled row
-          umma_tf32(tmem, a_hi + adv, b_hi + adv, idesc, (kb | kk) != 0 ? 1u : 0u);
-          umma_tf32(tmem, a_hi + adv, b_lo + adv, idesc, 1u);
-          umma_tf32(tmem, a_lo + adv, b_hi + adv, idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);  // 8 tf32 = 32 bytes along the swizzled row
+            umma_tf32(d, a_hi + adv, b_hi + adv, idesc, (first && kk == 0) ? 0u : 1u);
+            umma_tf32(d, a_hi + adv, b_lo + adv, idesc, 1u);
+            umma_tf32(d, a_lo + adv, b_hi + adv, idesc, 1u);
+          }
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&acc_full[buf]);
       }
-      umma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    // ---- converters: A -> (A_hi in place, A_lo) per stage ----
-    const int t = threadIdx.x - 64;  // 0..127
-    for (int kb = 0; kb < kblocks; ++kb) {
-      const int s = kb % Cfg::STAGES;
-      const uint32_t ph = (kb / Cfg::STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      float4* a = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES);
-      float4* alo = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES + A_BYTES);
+    // ---- workers (8 warps): convert A per stage; promote each finished
+    // TMEM chunk into round-to-nearest FP32 register accumulators; epilogue.
+    const int wt = threadIdx.x - 64;          // 0..255
+    const int quad = warp & 3;                // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;         // which half of the BN columns
+    float acc[HALF];
 #pragma unroll
-      for (int i = 0; i < A_BYTES / 16 / 128; ++i) {
-        const int idx = i * 128 + t;
-        const float4 x = a[idx];
-        float4 h, l;
-        h.x = tf32_rna(x.x); l.x = x.x - h.x;
-        h.y = tf32_rna(x.y); l.y = x.y - h.y;
-        h.z = tf32_rna(x.z); l.z = x.z - h.z;
-        h.w = tf32_rna(x.w); l.w = x.w - h.w;
-        a[idx] = h;
-        alo[idx] = l;
+    for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
+    // Chunk c's stages are converted first; then chunk c-1 (complete by
+    // then) is drained, freeing its TMEM buffer before the MMA needs it for
+    // chunk c+1.  One drain site keeps `acc` in registers.
+    for (int c = 0; c <= nchunks; ++c) {
+      if (c < nchunks) {
+        const int kb_end = min(kblocks, (c + 1) * kChunk);
+        for (int kb = c * kChunk; kb < kb_end; ++kb) {
+          const int s = kb % Cfg::STAGES;
+          const uint32_t ph = (kb / Cfg::STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          float4* a = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES);
+          float4* alo = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES + A_BYTES);
+#pragma unroll
+          for (int i = 0; i < A_BYTES / 16 / kWorkers; ++i) {
+            const int idx = i * kWorkers + wt;
+            const float4 x = a[idx];
+            float4 h, l;
+            h.x = tf32_rna(x.x); l.x = x.x - h.x;
+            h.y = tf32_rna(x.y); l.y = x.y - h.y;
+            h.z = tf32_rna(x.z); l.z = x.z - h.z;
+            h.w = tf32_rna(x.w); l.w = x.w - h.w;
+            a[idx] = h;
+            alo[idx] = l;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&conv[s]);
+        }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&conv[s]);
+      if (c >= 1) {
+        const int buf = (c - 1) & 1;
+        mbar_wait(&acc_full[buf], ((c - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < HALF / 16; ++j) {
+          float v[16];
+          tmem_ld16(lane_base + static_cast<uint32_t>(buf * BN + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(&acc_empty[buf]);
+      }
     }
+
     // ---- epilogue ----
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int row = quad * 32 + lane;
     const long long gm = m_tile * BM + row;
     const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
     const int shift = sa + sb;
     float local = 0.f;
-    float* crow = p.c + gm * p.n2 + static_cast<long long>(n_tile) * BN;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(quad * 32) << 16) + c0, v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = scalbnf(v[i], -shift);
+    for (int i = 0; i < HALF; ++i) acc[i] = scalbnf(acc[i], -shift);
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) local = fmaxf(local, v[i] * v[i] + v[i + 1] * v[i + 1]);
-      float4* dst = reinterpret_cast<float4*>(crow + c0);
+    for (int i = 0; i < HALF; i += 2) local = fmaxf(local, acc[i] * acc[i] + acc[i + 1] * acc[i + 1]);
+    float4* dst = reinterpret_cast<float4*>(p.c + gm * p.n2 + static_cast<long long>(n_tile) * BN + half * HALF);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) dst[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-    }
+    for (int i = 0; i < HALF / 4; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
     if (p.meta_c) {
       for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
       if (lane == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
@@ -401,9 +447,12 @@ bool tc_enabled() {
   return !(env && env[0] == '0');
 }
 
-bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool /*trans_b*/) {
-  if (!tc_enabled() || trans_a) return false;
-  if (m % BM != 0 || (2 * n) % 128 != 0 || (2 * k) % BK != 0) return false;
+bool cgemm_tc_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool /*trans_b*/) {
+  return !trans_a && m > 0 && m % BM == 0 && (2 * n) % 128 == 0 && n > 0 && (2 * k) % BK == 0 && k > 0;
+}
+
+bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
+  if (!tc_enabled() || !cgemm_tc_supported(m, n, k, trans_a, trans_b)) return false;
   // Worth it only for real work: >= ~1 GFLOP and a non-trivial K.
   return 8.0 * static_cast<double>(m) * n * k >= 1e9 && k >= 64;
 }
@@ -413,7 +462,8 @@ std::int64_t cgemm_tc_workspace_bytes(std::int64_t /*m*/, std::int64_t n, std::i
 }
 
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
-  if (!cgemm_tc_eligible(g.m, g.n, g.k, g.trans_a, g.trans_b)) throw std::invalid_argument("cgemm_tc: shape not eligible");
+  if (!cgemm_tc_supported(g.m, g.n, g.k, g.trans_a, g.trans_b))
+    throw std::invalid_argument("cgemm_tc: shape not supported by the tensor-core path");
   if (g.workspace == nullptr || g.workspace_bytes < cgemm_tc_workspace_bytes(g.m, g.n, g.k, g.trans_a, g.trans_b))
     throw std::invalid_argument("cgemm_tc: workspace too small");
   float* bhi = static_cast<float*>(g.workspace);

@@ -10,6 +10,9 @@
 namespace qsg::dev {
 
 // True when the shape/layout is handled by the tcgen05 kernel.
+// Layout constraints of the kernel (m % 128, n % 64, k % 16, A row-major).
+bool cgemm_tc_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
+// Supported and worth it (the engine uses this).
 bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
