@@ -146,6 +146,12 @@ int qsg_engine_create(const char* circuit_text, int kind, const char* plan_text,
                       int device, int flags, qsg_engine** out);
 int qsg_engine_destroy(qsg_engine* e);
 
+/* Compiles the device program for (circuit, plan) WITHOUT a device and
+ * returns its listing (ops, shapes, GEMM path, arena bytes) -- for planning
+ * and CPU-side checks.  Arguments as qsg_engine_create. */
+int qsg_program_listing(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                        int flags, char* buf, int64_t cap, int64_t* len);
+
 typedef struct qsg_engine_info {
   int64_t num_qubits, num_slices, batch_size, num_steps, max_rank;
   int64_t peak_memory;        /* reference annotate_plan prediction */

@@ -107,6 +107,7 @@ def lib():
         "qsg_normalize": (i32, [fp, i64, dp, P(i32)]),
         "qsg_engine_create": (i32, [cp, i32, cp, P(i32), i32, i32, i32, P(vp)]),
         "qsg_engine_destroy": (i32, [vp]),
+        "qsg_program_listing": (i32, [cp, i32, cp, P(i32), i32, i32, cp, i64, P(i64)]),
         "qsg_engine_get_info": (i32, [vp, P(_EngineInfo)]),
         "qsg_engine_plan_json": (i32, [vp, cp, i64, P(i64)]),
         "qsg_engine_describe": (i32, [vp, cp, i64, P(i64)]),
@@ -313,6 +314,14 @@ def normalize_inplace(data: np.ndarray, log_scale: float = 0.0):
     nz = C.c_int(0)
     _check(lib().qsg_normalize(_p(data.view(np.float32), C.c_float), data.size, C.byref(ls), C.byref(nz)))
     return bool(nz.value), ls.value
+
+
+def program_listing(circuit_text: str, plan_text: str = "", kind: int = PLAN_JSON, open_qubits=(),
+                    tensor_cores: bool = True) -> str:
+    """Device program the engine would run (no GPU needed): ops, GEMM shapes/paths, arena bytes."""
+    a, p = _i32(open_qubits)
+    return _text(lib().qsg_program_listing, circuit_text.encode(), kind, plan_text.encode(), p, len(a),
+                 0 if tensor_cores else 2)
 
 
 # ---- engine ---------------------------------------------------------------

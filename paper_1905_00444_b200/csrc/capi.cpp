@@ -443,6 +443,19 @@ int qsg_engine_create(const char* circuit_text, int kind, const char* plan_text,
   });
 }
 
+int qsg_program_listing(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                        int flags, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    const qsg::Circuit c = qsg::parse_circuit(circuit_text);
+    const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
+    qsg::EngineOptions o;
+    o.compile_only = true;
+    o.tensor_cores = (flags & QSG_ENGINE_NO_TENSOR_CORES) == 0;
+    qsg::Engine e(c, plan, o);
+    put_text(e.describe(), buf, cap, len);
+  });
+}
+
 int qsg_engine_destroy(qsg_engine* e) {
   return guarded([&] { delete e; });
 }

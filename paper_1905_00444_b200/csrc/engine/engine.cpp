@@ -73,8 +73,10 @@ bool seq_equal(const std::vector<Label>& a, std::size_t a0, const std::vector<La
 
 Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOptions& opt)
     : circuit_(c), plan_(plan), opt_(opt) {
-  check(cudaSetDevice(opt_.device), "cudaSetDevice");
-  check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (!opt_.compile_only) {
+    check(cudaSetDevice(opt_.device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  }
   // Node layout = fold layout (open label at axis 0, bonds in gate order).
   std::vector<int> x1(static_cast<std::size_t>(c.num_qubits()), 0);
   for (int q : plan_.open_qubits) x1[static_cast<std::size_t>(q)] = -1;
@@ -84,6 +86,9 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
   batch_ = std::int64_t{1} << plan_.open_qubits.size();
   compile();
   pack_buffers();
+  op_ms_.assign(ops_.size(), 0.0);
+  op_execs_.assign(ops_.size(), 0);
+  if (opt_.compile_only) return;  // program listing only (no device)
   check(cudaMalloc(&arena_, static_cast<std::size_t>(std::max<std::int64_t>(arena_bytes_, kAlign))), "arena cudaMalloc");
   check(cudaMalloc(&metas_, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta cudaMalloc");
   check(cudaMemset(metas_, 0, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta memset");
@@ -107,6 +112,7 @@ void Engine::set_profile(bool on) {
 }
 
 Engine::~Engine() {
+  if (opt_.compile_only) return;
   cudaSetDevice(opt_.device);
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto e : ev_) cudaEventDestroy(e);
@@ -206,74 +212,103 @@ void Engine::compile() {
     live.erase(li);
     live.erase(step.rhs);
 
-    std::vector<Label> con_l, con_r, lfree, rfree;
-    for (const auto& l : L.labels) (R.has(l) ? con_l : lfree).push_back(l);
-    for (const auto& l : R.labels) (L.has(l) ? con_r : rfree).push_back(l);
-    std::int64_t m = 1, nn = 1, k = 1;
-    for (const auto& l : lfree) m *= L.dim_of(l);
-    for (const auto& l : rfree) nn *= R.dim_of(l);
-    for (const auto& l : con_l) {
-      if (L.dim_of(l) != R.dim_of(l)) throw std::invalid_argument("contract: extent mismatch on " + l);
-      k *= L.dim_of(l);
-    }
+    std::int64_t k = 1;
+    std::vector<Label> con_l;
+    for (const auto& l : L.labels)
+      if (R.has(l)) {
+        if (L.dim_of(l) != R.dim_of(l)) throw std::invalid_argument("contract: extent mismatch on " + l);
+        con_l.push_back(l);
+        k *= L.dim_of(l);
+      }
+    std::vector<Label> con_r;
+    for (const auto& l : R.labels)
+      if (L.has(l)) con_r.push_back(l);
+    const std::int64_t ml = L.volume() / k, nr = R.volume() / k;
     constexpr std::int64_t kMaxVolume = std::int64_t{1} << 33;  // contraction.hpp:95, :189-191
-    if (m * k > kMaxVolume || k * nn > kMaxVolume || m * nn > kMaxVolume)
+    if (ml * k > kMaxVolume || k * nr > kMaxVolume || ml * nr > kMaxVolume)
       throw std::length_error("contract_ttgt: volume overflow");
 
-    // Layout choice: contracted order taken from L or from R; an operand is
-    // used in place when dense with the contracted labels as a suffix/prefix.
+    // Operand roles and layouts, by a time model.  C = [A free, B free];
+    // either L or R takes the A role (streamed, rows of C), the contracted
+    // order comes from either operand, and an operand is used in place when
+    // dense with the contracted labels as a suffix/prefix (A: N or T, B: N
+    // or T) -- otherwise K1 permutes it to the N layout.  The tcgen05 GEMM
+    // needs A in N layout and expands B (40 B per element), so forcing a
+    // permute of A can pay for itself on large steps.
     struct Choice {
+      bool swap = false, use_a = false, ta = false, use_b = false, tb = false, tc = false;
       std::vector<Label> con;
-      bool use_a = false, ta = false, use_b = false, tb = false;
-      std::int64_t cost = 0;
+      double cost = 0.0;
     };
-    auto evaluate = [&](const std::vector<Label>& con) {
+    const double flops = static_cast<double>(step.flops);
+    constexpr double kHbm = 5.0e12, kTcRate = 1.5e14, kSimtRate = 4.0e13;
+    constexpr std::int64_t kMaxTcWorkspace = std::int64_t{48} << 30;  // B_r^T hi+lo = 32 B per B element
+    auto evaluate = [&](bool swap, const std::vector<Label>& con, bool force_permute_a) {
+      const View& X = swap ? R : L;
+      const View& Y = swap ? L : R;
       Choice ch;
+      ch.swap = swap;
       ch.con = con;
       const std::size_t nc = con.size();
-      if (L.dense()) {
-        if (seq_equal(L.labels, L.labels.size() - nc, con)) { ch.use_a = true; ch.ta = false; }
-        else if (seq_equal(L.labels, 0, con)) { ch.use_a = true; ch.ta = true; }
+      if (X.dense() && !force_permute_a) {
+        if (seq_equal(X.labels, X.labels.size() - nc, con)) { ch.use_a = true; ch.ta = false; }
+        else if (seq_equal(X.labels, 0, con)) { ch.use_a = true; ch.ta = true; }
       }
-      if (R.dense()) {
-        if (seq_equal(R.labels, 0, con)) { ch.use_b = true; ch.tb = false; }
-        else if (seq_equal(R.labels, R.labels.size() - nc, con)) { ch.use_b = true; ch.tb = true; }
+      if (Y.dense()) {
+        if (seq_equal(Y.labels, 0, con)) { ch.use_b = true; ch.tb = false; }
+        else if (seq_equal(Y.labels, Y.labels.size() - nc, con)) { ch.use_b = true; ch.tb = true; }
       }
-      ch.cost = (ch.use_a ? 0 : L.volume()) + (ch.use_b ? 0 : R.volume());
+      const std::int64_t mm = X.volume() / k, nn2 = Y.volume() / k;
+      const bool ta = ch.use_a && ch.ta, tb = ch.use_b && ch.tb;
+      ch.tc = opt_.tensor_cores && dev::cgemm_tc_eligible(mm, nn2, k, ta, tb) &&
+              dev::cgemm_tc_workspace_bytes(mm, nn2, k, ta, tb) <= kMaxTcWorkspace;
+      const double bytes = (ch.use_a ? 0.0 : 16.0 * X.volume()) + (ch.use_b ? 0.0 : 16.0 * Y.volume()) +
+                           (ch.tc ? 40.0 * Y.volume() : 0.0);
+      ch.cost = bytes / kHbm + flops / (ch.tc ? kTcRate : kSimtRate);
       return ch;
     };
-    Choice best = evaluate(con_l);
-    Choice alt = evaluate(con_r);
-    if (alt.cost < best.cost) best = alt;
+    Choice best = evaluate(false, con_l, false);
+    for (bool swap : {false, true})
+      for (const auto* con : {&con_l, &con_r})
+        for (bool force : {false, true}) {
+          Choice c = evaluate(swap, *con, force);
+          if (c.cost < best.cost) best = c;
+        }
 
-    const int op_first = static_cast<int>(ops_.size());
-    View A = L, B = R;
+    const View& X = best.swap ? R : L;
+    const View& Y = best.swap ? L : R;
+    std::vector<Label> xfree, yfree;
+    for (const auto& l : X.labels)
+      if (!Y.has(l)) xfree.push_back(l);
+    for (const auto& l : Y.labels)
+      if (!X.has(l)) yfree.push_back(l);
+    View A = X, B = Y;
     if (!best.use_a) {
-      std::vector<Label> order = lfree;
+      std::vector<Label> order = xfree;
       order.insert(order.end(), best.con.begin(), best.con.end());
-      A = permute_to(L, order, static_cast<int>(si));
+      A = permute_to(X, order, static_cast<int>(si));
       best.ta = false;
     }
     if (!best.use_b) {
       std::vector<Label> order = best.con;
-      order.insert(order.end(), rfree.begin(), rfree.end());
-      B = permute_to(R, order, static_cast<int>(si));
+      order.insert(order.end(), yfree.begin(), yfree.end());
+      B = permute_to(Y, order, static_cast<int>(si));
       best.tb = false;
     }
     // Free-label orders as laid out in the operands.
     std::vector<Label> a_free, b_free;
     for (const auto& l : A.labels)
-      if (!R.has(l)) a_free.push_back(l);
+      if (!Y.has(l)) a_free.push_back(l);
     for (const auto& l : B.labels)
-      if (!L.has(l)) b_free.push_back(l);
+      if (!X.has(l)) b_free.push_back(l);
 
     Op g;
     g.kind = 1;
     g.step = static_cast<int>(si);
     g.a = as_operand(A);
     g.b = as_operand(B);
-    g.m = m;
-    g.n = nn;
+    g.m = X.volume() / k;
+    g.n = Y.volume() / k;
     g.k = k;
     g.ta = best.ta;
     g.tb = best.tb;
@@ -281,14 +316,14 @@ void Engine::compile() {
     g.meta_b = B.meta;
     g.meta_c = static_cast<int>(si);
     g.flops = step.flops;
-    g.tc = opt_.tensor_cores && dev::cgemm_tc_eligible(m, nn, k, g.ta, g.tb);
-    g.ws_bytes = g.tc ? dev::cgemm_tc_workspace_bytes(m, nn, k, g.ta, g.tb) : dev::cgemm_workspace_bytes(m, nn, k);
+    g.tc = opt_.tensor_cores && dev::cgemm_tc_eligible(g.m, g.n, k, g.ta, g.tb) &&
+           dev::cgemm_tc_workspace_bytes(g.m, g.n, k, g.ta, g.tb) <= kMaxTcWorkspace;
+    g.ws_bytes = g.tc ? dev::cgemm_tc_workspace_bytes(g.m, g.n, k, g.ta, g.tb) : dev::cgemm_workspace_bytes(g.m, g.n, k);
     touch(A.buf);
     touch(B.buf);
-    g.c = new_buf(m * nn * 8);
+    g.c = new_buf(g.m * g.n * 8);
     if (g.ws_bytes > 0) g.ws = new_buf(g.ws_bytes);
     ops_.push_back(g);
-    (void)op_first;
 
     View C;
     C.buf = g.c;
@@ -527,8 +562,8 @@ std::string Engine::describe() const {
   for (const auto& op : ops_) {
     if (op.kind == 0) os << "  permute step " << op.step << " elems " << op.count << " rank " << op.ext.size() << "\n";
     else if (op.kind == 1)
-      os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << (op.ta ? " TA" : "")
-         << (op.tb ? " TB" : "") << (op.tc ? " tc" : "") << "\n";
+      os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << " flops " << op.flops
+         << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes << "\n";
     else os << "  accumulate " << op.count << "\n";
   }
   return os.str();

@@ -36,6 +36,7 @@ struct EngineOptions {
   int device = 0;
   bool profile = false;     // CUDA events around every kernel op
   bool tensor_cores = true; // allow the tcgen05 GEMM for eligible steps
+  bool compile_only = false; // build the program listing without touching a device
 };
 
 struct OpProfile {
