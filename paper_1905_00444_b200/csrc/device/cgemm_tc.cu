@@ -89,6 +89,7 @@ struct TcParams {
   const TMeta* meta_b;
   TMeta* meta_c;
   int norm_a, norm_b;
+  int raw_hi;  // experiment: feed raw fp32 as the hi part (valid iff the tensor core truncates)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -160,6 +161,8 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t u;
@@ -302,11 +305,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int idx = i * kWorkers + wt;
             const float4 x = a[idx];
             float4 h, l;
-            h.x = tf32_rna(x.x); l.x = x.x - h.x;
-            h.y = tf32_rna(x.y); l.y = x.y - h.y;
-            h.z = tf32_rna(x.z); l.z = x.z - h.z;
-            h.w = tf32_rna(x.w); l.w = x.w - h.w;
-            a[idx] = h;
+            if (p.raw_hi) {
+              l.x = x.x - tf32_trunc(x.x);
+              l.y = x.y - tf32_trunc(x.y);
+              l.z = x.z - tf32_trunc(x.z);
+              l.w = x.w - tf32_trunc(x.w);
+            } else {
+              h.x = tf32_rna(x.x); l.x = x.x - h.x;
+              h.y = tf32_rna(x.y); l.y = x.y - h.y;
+              h.z = tf32_rna(x.z); l.z = x.z - h.z;
+              h.w = tf32_rna(x.w); l.w = x.w - h.w;
+              a[idx] = h;
+            }
             alo[idx] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -359,7 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // B (complex, [k][n] or [n][k]) -> B_r^T hi/lo planes [2n][2k] fp32.
 __global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict__ b, float* __restrict__ hi,
-                                                        float* __restrict__ lo, long long n, long long k, int tb) {
+                                                        float* __restrict__ lo, long long n, long long k, int tb,
+                                                        int raw_hi) {
   __shared__ float2 tile[32][33];  // [p_local][j_local]
   const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -381,13 +392,22 @@ __global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict
     const float re = v.x, im = v.y;
     float h0, h1, h2, h3;
     uint32_t u;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(re)); h0 = __uint_as_float(u);
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(-im)); h1 = __uint_as_float(u);
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(im)); h2 = __uint_as_float(u);
+    if (raw_hi) {
+      h0 = tf32_trunc(re); h1 = tf32_trunc(-im); h2 = tf32_trunc(im);
+    } else {
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(re)); h0 = __uint_as_float(u);
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(-im)); h1 = __uint_as_float(u);
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(im)); h2 = __uint_as_float(u);
+    }
     h3 = h0;
     const long long row0 = (2 * j) * k2 + 2 * p, row1 = (2 * j + 1) * k2 + 2 * p;
-    *reinterpret_cast<float2*>(hi + row0) = make_float2(h0, h1);
-    *reinterpret_cast<float2*>(hi + row1) = make_float2(h2, h3);
+    if (raw_hi) {
+      *reinterpret_cast<float2*>(hi + row0) = make_float2(re, -im);
+      *reinterpret_cast<float2*>(hi + row1) = make_float2(im, re);
+    } else {
+      *reinterpret_cast<float2*>(hi + row0) = make_float2(h0, h1);
+      *reinterpret_cast<float2*>(hi + row1) = make_float2(h2, h3);
+    }
     *reinterpret_cast<float2*>(lo + row0) = make_float2(re - h0, -im - h1);
     *reinterpret_cast<float2*>(lo + row1) = make_float2(im - h2, re - h3);
   }
@@ -423,6 +443,11 @@ CUtensorMap make_map(const void* base, long long cols, long long rows, int box_r
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
+}
+
+bool raw_hi_mode() {
+  const char* env = std::getenv("QSG_TC_RAWHI");
+  return env && env[0] == '1';
 }
 
 int tc_bn(std::int64_t n) {
@@ -470,7 +495,8 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
   float* blo = bhi + (2 * g.n) * (2 * g.k);
   {
     dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
-    tc_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k, g.trans_b ? 1 : 0);
+    tc_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k, g.trans_b ? 1 : 0,
+                                                raw_hi_mode() ? 1 : 0);
     if (launches) ++*launches;
   }
   const int bn = tc_bn(g.n);
@@ -487,6 +513,7 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
   p.meta_c = g.meta_c;
   p.norm_a = g.norm_a;
   p.norm_b = g.norm_b;
+  p.raw_hi = raw_hi_mode() ? 1 : 0;
   const long long mt = g.m / BM, nt = (2 * g.n) / bn;
   if (mt * nt > 2147483647LL || g.m > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
   p.n_tiles = static_cast<int>(nt);
