@@ -367,6 +367,255 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 2-CTA variant (cta_group::2): a CTA pair computes a 256 x 256 (real) output
+// tile with M=256 UMMAs issued by the leader.  Each CTA stages ITS 128 rows
+// of A and ITS half (128 rows of B_r^T) of B, so per-SM shared-memory and
+// L2 traffic per MMA drop by a third/half against the 1-CTA kernel and a
+// third pipeline stage fits (64 KiB per stage).  Each CTA's TMEM holds its
+// 128 output rows x 256 columns (x2 chunk buffers = 512 columns).
+// Barriers: full[] and the TMEM-chunk acc_full[] are per CTA; conv[] and
+// acc_empty[] live in the leader and collect arrivals from both CTAs'
+// workers (remote mbarrier arrive over the cluster); the leader's
+// tcgen05.commit multicasts to both CTAs.
+constexpr int kPairBN = 256;  // real output columns per CTA pair
+struct Tc2Cfg {
+  static constexpr int A_B = BM * BK * 4;            // this CTA's 128 rows of A
+  static constexpr int B_B = (kPairBN / 2) * BK * 4; // this CTA's half of B_r^T
+  static constexpr int STAGE_BYTES = 2 * A_B + 2 * B_B;
+  static constexpr int STAGES = 3;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * kPairBN;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Arrive on the barrier at the same smem offset in cluster CTA `cta`.
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma2_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3))
+      : "memory");
+}
+
+__host__ __device__ constexpr uint32_t tf32_idesc_pair() {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kPairBN >> 3) << 17) |
+         (static_cast<uint32_t>(256 >> 4) << 24);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    cgemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
+                     const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
+  using Cfg = Tc2Cfg;
+  constexpr int HALF = kPairBN / 2;  // accumulator columns per worker thread
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* conv = full + Cfg::STAGES;
+  uint64_t* empty = conv + Cfg::STAGES;
+  uint64_t* acc_full = empty + Cfg::STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const long long pair = blockIdx.x >> 1;
+  const int n_tile = static_cast<int>(pair % p.n_tiles);
+  const long long m_pair = pair / p.n_tiles;
+  const long long row0 = m_pair * 256 + static_cast<long long>(rank) * BM;  // this CTA's rows of A / C
+  const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);  // this CTA's rows of B_r^T
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 2 * kWorkers);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 2 * kWorkers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_bhi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_blo) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "n"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_slot;
+  const int kblocks = p.kblocks;
+  const int nchunks = (kblocks + kChunk - 1) / kChunk;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < kblocks; ++kb) {
+        const int s = kb % Cfg::STAGES;
+        const uint32_t ph = (kb / Cfg::STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+        mbar_expect_tx(&full[s], Cfg::A_B + 2 * Cfg::B_B);
+        tma_load_2d(&map_a, &full[s], st, kb * BK, static_cast<int>(row0));
+        tma_load_2d(&map_bhi, &full[s], st + 2 * Cfg::A_B, kb * BK, brow0);
+        tma_load_2d(&map_blo, &full[s], st + 2 * Cfg::A_B + Cfg::B_B, kb * BK, brow0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = tf32_idesc_pair();
+      for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        mbar_wait_cluster(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
+        const int kb_end = min(kblocks, (c + 1) * kChunk);
+        for (int kb = c * kChunk; kb < kb_end; ++kb) {
+          const int s = kb % Cfg::STAGES;
+          const uint32_t ph = (kb / Cfg::STAGES) & 1;
+          mbar_wait_cluster(&conv[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          const uint64_t a_hi = kmajor_sw128_desc(smem_u32(st));
+          const uint64_t a_lo = kmajor_sw128_desc(smem_u32(st + Cfg::A_B));
+          const uint64_t b_hi = kmajor_sw128_desc(smem_u32(st + 2 * Cfg::A_B));
+          const uint64_t b_lo = kmajor_sw128_desc(smem_u32(st + 2 * Cfg::A_B + Cfg::B_B));
+          const bool first = kb == c * kChunk;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);
+            umma2_tf32(d, a_hi + adv, b_hi + adv, idesc, (first && kk == 0) ? 0u : 1u);
+            umma2_tf32(d, a_hi + adv, b_lo + adv, idesc, 1u);
+            umma2_tf32(d, a_lo + adv, b_hi + adv, idesc, 1u);
+          }
+          umma2_commit_both(&empty[s]);
+        }
+        umma2_commit_both(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int wt = threadIdx.x - 64;
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    float acc[HALF];
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
+    for (int c = 0; c <= nchunks; ++c) {
+      if (c < nchunks) {
+        const int kb_end = min(kblocks, (c + 1) * kChunk);
+        for (int kb = c * kChunk; kb < kb_end; ++kb) {
+          const int s = kb % Cfg::STAGES;
+          const uint32_t ph = (kb / Cfg::STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          float4* a = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES);
+          float4* alo = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_B);
+#pragma unroll
+          for (int i = 0; i < Cfg::A_B / 16 / kWorkers; ++i) {
+            const int idx = i * kWorkers + wt;
+            const float4 x = a[idx];
+            float4 h, l;
+            if (p.raw_hi) {
+              l.x = x.x - tf32_trunc(x.x);
+              l.y = x.y - tf32_trunc(x.y);
+              l.z = x.z - tf32_trunc(x.z);
+              l.w = x.w - tf32_trunc(x.w);
+            } else {
+              h.x = tf32_rna(x.x); l.x = x.x - h.x;
+              h.y = tf32_rna(x.y); l.y = x.y - h.y;
+              h.z = tf32_rna(x.z); l.z = x.z - h.z;
+              h.w = tf32_rna(x.w); l.w = x.w - h.w;
+              a[idx] = h;
+            }
+            alo[idx] = l;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_remote(&conv[s], 0);
+        }
+      }
+      if (c >= 1) {
+        const int buf = (c - 1) & 1;
+        mbar_wait(&acc_full[buf], ((c - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < HALF / 16; ++j) {
+          float v[16];
+          tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive_remote(&acc_empty[buf], 0);
+      }
+    }
+    const long long gm = row0 + quad * 32 + lane;
+    const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
+    const int shift = sa + sb;
+    float local = 0.f;
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) acc[i] = scalbnf(acc[i], -shift);
+#pragma unroll
+    for (int i = 0; i < HALF; i += 2) local = fmaxf(local, acc[i] * acc[i] + acc[i + 1] * acc[i + 1]);
+    float4* dst = reinterpret_cast<float4*>(p.c + gm * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF);
+#pragma unroll
+    for (int i = 0; i < HALF / 4; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+    if (p.meta_c) {
+      for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+      if (lane == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
+      if (blockIdx.x == 0 && threadIdx.x == 64)
+        p.meta_c->log_scale = (p.meta_a ? p.meta_a->log_scale : 0.0) + (p.meta_b ? p.meta_b->log_scale : 0.0) + shift;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
+  }
+}
+
 // B (complex, [k][n] or [n][k]) -> B_r^T hi/lo planes [2n][2k] fp32.
 __global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict__ b, float* __restrict__ hi,
                                                         float* __restrict__ lo, long long n, long long k, int tb,
@@ -450,6 +699,13 @@ bool raw_hi_mode() {
   return env && env[0] == '1';
 }
 
+// The CTA-pair kernel covers 256 x 256 (real) tiles; QSG_TC_2SM=0 disables it.
+bool use_pair(std::int64_t m, std::int64_t n) {
+  const char* env = std::getenv("QSG_TC_2SM");
+  if (env && env[0] == '0') return false;
+  return m % 256 == 0 && (2 * n) % kPairBN == 0;
+}
+
 int tc_bn(std::int64_t n) {
   const char* env = std::getenv("QSG_TC_BN");
   const int want = env ? std::atoi(env) : 256;
@@ -498,6 +754,32 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     tc_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k, g.trans_b ? 1 : 0,
                                                 raw_hi_mode() ? 1 : 0);
     if (launches) ++*launches;
+  }
+  if (use_pair(g.m, g.n)) {
+    const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
+    const CUtensorMap mbh = make_map(bhi, 2 * g.k, 2 * g.n, kPairBN / 2);
+    const CUtensorMap mbl = make_map(blo, 2 * g.k, 2 * g.n, kPairBN / 2);
+    TcParams p{};
+    p.c = static_cast<float*>(g.c);
+    p.m = g.m;
+    p.n2 = 2 * g.n;
+    p.kblocks = static_cast<int>((2 * g.k) / BK);
+    p.meta_a = g.meta_a;
+    p.meta_b = g.meta_b;
+    p.meta_c = g.meta_c;
+    p.norm_a = g.norm_a;
+    p.norm_b = g.norm_b;
+    p.raw_hi = raw_hi_mode() ? 1 : 0;
+    const long long pairs = (g.m / 256) * ((2 * g.n) / kPairBN);
+    if (2 * pairs > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
+    p.n_tiles = static_cast<int>((2 * g.n) / kPairBN);
+    static std::once_flag once;
+    std::call_once(once, [] {
+      cudaFuncSetAttribute(cgemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg::SMEM);
+    });
+    cgemm_tc2_kernel<<<static_cast<unsigned>(2 * pairs), kThreads, Tc2Cfg::SMEM, stream>>>(ma, mbh, mbl, p);
+    if (launches) ++*launches;
+    return cudaGetLastError();
   }
   const int bn = tc_bn(g.n);
   const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);

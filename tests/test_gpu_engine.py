@@ -141,3 +141,31 @@ def test_engine_rejects_bad_inputs(gpu, cases):
         bad[case["open"][0]] = 0
         with pytest.raises(gpu.InvalidArgument):
             e.prepare(bad)
+
+
+def test_config2_full_size_tensor_core_vs_simt(gpu):
+    """BASELINE config 2 at full size (7x7, 1+32+1, 1024-amplitude batch, 2
+    slices, 2.15e14 flop): the tcgen05 3xTF32 engine and the FP32-FFMA
+    engine are independent GEMM implementations; they must agree within the
+    north-star tolerance (1e-4 on |amp|, batch fidelity >= 1 - 1e-6).  Also
+    checks the size-independent properties: Porter-Thomas scale of the batch
+    norm and cut completeness (per-slice contributions sum to the batch)."""
+    text = gpu.generate_rqc(7, 7, 32, 0)
+    plan = open(os.path.join(ROOT, "configs", "config2_plan.json")).read()
+    opn = json.loads(plan)["open_qubits"]
+    x1 = gpu.draw_x1(49, opn, 0, 0)
+    res = {}
+    for tc in (True, False):
+        with gpu.Engine(text, plan, tensor_cores=tc) as e:
+            e.prepare(x1)
+            e.run([0, 1], reset=True, per_slice=True)
+            res[tc] = e.results()
+    (a, pa), (b, pb) = res[True], res[False]
+    assert np.array_equal(pa[0] + pa[1], a) and np.array_equal(pb[0] + pb[1], b)
+    big = np.abs(b) > 0.1 * np.abs(b).mean()  # relative |amp| check above a magnitude floor
+    assert np.max(np.abs(np.abs(a[big]) - np.abs(b[big])) / np.abs(b[big])) < 1e-4
+    assert rel(a, b) < 1e-4
+    fid = abs(np.vdot(a, b)) ** 2 / (np.vdot(a, a).real * np.vdot(b, b).real)
+    assert fid >= 1 - 1e-6
+    # Porter-Thomas: E[2^n |a|^2] = 1 over random bitstrings (loose, 1024 samples)
+    assert 0.8 < np.mean(np.abs(a) ** 2) * 2.0**49 < 1.25
