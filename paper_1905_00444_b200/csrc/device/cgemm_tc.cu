@@ -20,7 +20,8 @@
 //
 // Accumulation: the tensor core's FP32 accumulator truncates, so its error
 // grows linearly with K (measured 9e-4 at K=65536).  Partial sums are
-// therefore promoted every kChunk k-blocks (32 complex K) from a
+// therefore promoted every 4 k-blocks (64 complex K; measured error
+// ~1e-6 up to K=65536, vs 6.5e-6 for FP32 FFMA) from a
 // double-buffered TMEM accumulator into round-to-nearest FP32 registers,
 // overlapping the MMA of the next chunk (cf. DeepSeek-V3's FP8 promotion).
 //
@@ -68,7 +69,7 @@ constexpr int kThreads = 64 + kWorkers;   // + producer warp + MMA warp
 // registers: the tensor core's FP32 accumulator truncates, so its error
 // grows linearly with the reduction length (measured ~1.4e-8 * k); 32
 // complex K per chunk keeps it at the 3xTF32 floor (~5e-7).
-constexpr int kChunk = 2;
+constexpr int kChunkDefault = 4;  // QSG_TC_CHUNK overrides (experiments)
 constexpr int A_BYTES = BM * BK * 4;
 
 template <int BN>
@@ -89,6 +90,7 @@ struct TcParams {
   const TMeta* meta_b;
   TMeta* meta_c;
   int norm_a, norm_b;
+  int chunk;   // k-blocks per TMEM promotion chunk
   int raw_hi;  // experiment: feed raw fp32 as the hi part (valid iff the tensor core truncates)
 };
 
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_slot;
   const int kblocks = p.kblocks;
-  const int nchunks = (kblocks + kChunk - 1) / kChunk;
+  const int nchunks = (kblocks + p.chunk - 1) / p.chunk;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -253,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + static_cast<uint32_t>(buf * BN);
-        const int kb_end = min(kblocks, (c + 1) * kChunk);
-        for (int kb = c * kChunk; kb < kb_end; ++kb) {
+        const int kb_end = min(kblocks, (c + 1) * p.chunk);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
           const int s = kb % Cfg::STAGES;
           const uint32_t ph = (kb / Cfg::STAGES) & 1;
           mbar_wait(&conv[s], ph);
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t a_lo = kmajor_sw128_desc(smem_u32(st + A_BYTES));
           const uint64_t b_hi = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES));
           const uint64_t b_lo = kmajor_sw128_desc(smem_u32(st + 2 * A_BYTES + Cfg::B_BYTES));
-          const bool first = kb == c * kChunk;
+          const bool first = kb == c * p.chunk;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);  // 8 tf32 = 32 bytes along the swizzled row
@@ -293,8 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // chunk c+1.  One drain site keeps `acc` in registers.
     for (int c = 0; c <= nchunks; ++c) {
       if (c < nchunks) {
-        const int kb_end = min(kblocks, (c + 1) * kChunk);
-        for (int kb = c * kChunk; kb < kb_end; ++kb) {
+        const int kb_end = min(kblocks, (c + 1) * p.chunk);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
           const int s = kb % Cfg::STAGES;
           const uint32_t ph = (kb / Cfg::STAGES) & 1;
           mbar_wait(&full[s], ph);
@@ -379,6 +381,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // workers (remote mbarrier arrive over the cluster); the leader's
 // tcgen05.commit multicasts to both CTAs.
 constexpr int kPairBN = 256;  // real output columns per CTA pair
+constexpr int kGroupM = 8;    // m-pairs per rasterization group
 struct Tc2Cfg {
   static constexpr int A_B = BM * BK * 4;            // this CTA's 128 rows of A
   static constexpr int B_B = (kPairBN / 2) * BK * 4; // this CTA's half of B_r^T
@@ -403,6 +406,13 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) 
   uint32_t ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(cta));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+// Warp-aggregated arrival on the leader's barrier: the leader's own warps
+// arrive locally (CTA scope), the peer's remotely (release.cluster).
+__device__ __forceinline__ void arrive_leader(uint64_t* bar, uint32_t rank) {
+  if (rank == 0) mbar_arrive(bar);
+  else mbar_arrive_remote(bar, 0);
 }
 
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
@@ -437,6 +447,24 @@ __host__ __device__ constexpr uint32_t tf32_idesc_pair() {
          (static_cast<uint32_t>(256 >> 4) << 24);
 }
 
+// Grouped rasterization of pair tiles: pairs running concurrently cover a
+// kGroupM x (clusters/kGroupM) block of (m, n) tiles, so the A rows and the
+// expanded-B columns they stream are shared through L2 (n-fastest order
+// re-read all of B_r^T from HBM per wave of m tiles: 1.2 TB per s026 launch).
+__device__ __forceinline__ void pair_tile_coords(long long t, long long m_pairs, int n_tiles, long long& m_pair,
+                                                 int& n_tile) {
+  const long long span = static_cast<long long>(kGroupM) * n_tiles;
+  const long long first_m = (t / span) * kGroupM;
+  const long long gsize = min(static_cast<long long>(kGroupM), m_pairs - first_m);
+  const long long within = t % span;
+  m_pair = first_m + within % gsize;
+  n_tile = static_cast<int>(within / gsize);
+}
+
+// Persistent: each CTA pair walks tiles t = cluster, cluster + nclusters, ...
+// with pipeline counters that run across tile boundaries, so TMA prefetch,
+// conversion and MMA of the next tile overlap the epilogue of the previous
+// one and the per-tile setup (barriers, TMEM allocation) is paid once.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cgemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
@@ -454,21 +482,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
-  const long long pair = blockIdx.x >> 1;
-  const int n_tile = static_cast<int>(pair % p.n_tiles);
-  const long long m_pair = pair / p.n_tiles;
-  const long long row0 = m_pair * 256 + static_cast<long long>(rank) * BM;  // this CTA's rows of A / C
-  const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);  // this CTA's rows of B_r^T
+  const long long cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const long long m_pairs = p.m / 256;
+  const long long total = m_pairs * p.n_tiles;
+  const long long my_tiles = cluster < total ? (total - 1 - cluster) / nclusters + 1 : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 2 * kWorkers);
+      mbar_init(&conv[s], 2 * kWorkers / 32);  // one arrival per worker warp of each CTA
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 2 * kWorkers);
+      mbar_init(&acc_empty[b], 2 * kWorkers / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -487,33 +514,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_slot;
   const int kblocks = p.kblocks;
-  const int nchunks = (kblocks + kChunk - 1) / kChunk;
+  const int nchunks = (kblocks + p.chunk - 1) / p.chunk;
+  const long long total_chunks = my_tiles * nchunks;
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < kblocks; ++kb) {
-        const int s = kb % Cfg::STAGES;
-        const uint32_t ph = (kb / Cfg::STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* st = smem + s * Cfg::STAGE_BYTES;
-        mbar_expect_tx(&full[s], Cfg::A_B + 2 * Cfg::B_B);
-        tma_load_2d(&map_a, &full[s], st, kb * BK, static_cast<int>(row0));
-        tma_load_2d(&map_bhi, &full[s], st + 2 * Cfg::A_B, kb * BK, brow0);
-        tma_load_2d(&map_blo, &full[s], st + 2 * Cfg::A_B + Cfg::B_B, kb * BK, brow0);
+      long long g = 0;  // k-block counter across tiles
+      for (long long ti = 0; ti < my_tiles; ++ti) {
+        long long m_pair;
+        int n_tile;
+        pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
+        const int row0 = static_cast<int>(m_pair * 256 + static_cast<long long>(rank) * BM);
+        const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);
+        for (int kb = 0; kb < kblocks; ++kb, ++g) {
+          const int s = static_cast<int>(g % Cfg::STAGES);
+          const uint32_t ph = static_cast<uint32_t>((g / Cfg::STAGES) & 1);
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          mbar_expect_tx(&full[s], Cfg::A_B + 2 * Cfg::B_B);
+          tma_load_2d(&map_a, &full[s], st, kb * BK, row0);
+          tma_load_2d(&map_bhi, &full[s], st + 2 * Cfg::A_B, kb * BK, brow0);
+          tma_load_2d(&map_blo, &full[s], st + 2 * Cfg::A_B + Cfg::B_B, kb * BK, brow0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = tf32_idesc_pair();
-      for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        mbar_wait_cluster(&acc_empty[buf], ((c >> 1) & 1) ^ 1);
+      long long g = 0;
+      for (long long q = 0; q < total_chunks; ++q) {
+        const int c = static_cast<int>(q % nchunks);
+        const int buf = static_cast<int>(q & 1);
+        mbar_wait_cluster(&acc_empty[buf], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
-        const int kb_end = min(kblocks, (c + 1) * kChunk);
-        for (int kb = c * kChunk; kb < kb_end; ++kb) {
-          const int s = kb % Cfg::STAGES;
-          const uint32_t ph = (kb / Cfg::STAGES) & 1;
+        const int kb_end = min(kblocks, (c + 1) * p.chunk);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb, ++g) {
+          const int s = static_cast<int>(g % Cfg::STAGES);
+          const uint32_t ph = static_cast<uint32_t>((g / Cfg::STAGES) & 1);
           mbar_wait_cluster(&conv[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
@@ -521,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const uint64_t a_lo = kmajor_sw128_desc(smem_u32(st + Cfg::A_B));
           const uint64_t b_hi = kmajor_sw128_desc(smem_u32(st + 2 * Cfg::A_B));
           const uint64_t b_lo = kmajor_sw128_desc(smem_u32(st + 2 * Cfg::A_B + Cfg::B_B));
-          const bool first = kb == c * kChunk;
+          const bool first = kb == c * p.chunk;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);
@@ -543,12 +581,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
-    for (int c = 0; c <= nchunks; ++c) {
-      if (c < nchunks) {
-        const int kb_end = min(kblocks, (c + 1) * kChunk);
-        for (int kb = c * kChunk; kb < kb_end; ++kb) {
-          const int s = kb % Cfg::STAGES;
-          const uint32_t ph = (kb / Cfg::STAGES) & 1;
+    const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
+    const int shift = sa + sb;
+    float local = 0.f;
+    long long g = 0;
+    // Flat software pipeline over this pair's chunks: convert chunk q, then
+    // promote chunk q-1 (complete by then), and after a tile's last chunk
+    // write its epilogue -- the MMA meanwhile works on the next tile.
+    for (long long q = 0; q <= total_chunks; ++q) {
+      if (q < total_chunks) {
+        const int c = static_cast<int>(q % nchunks);
+        const int kb_end = min(kblocks, (c + 1) * p.chunk);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb, ++g) {
+          const int s = static_cast<int>(g % Cfg::STAGES);
+          const uint32_t ph = static_cast<uint32_t>((g / Cfg::STAGES) & 1);
           mbar_wait(&full[s], ph);
           float4* a = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES);
           float4* alo = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_B);
@@ -572,12 +618,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             alo[idx] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive_remote(&conv[s], 0);
+          __syncwarp();
+          if (lane == 0) arrive_leader(&conv[s], rank);
         }
       }
-      if (c >= 1) {
-        const int buf = (c - 1) & 1;
-        mbar_wait(&acc_full[buf], ((c - 1) >> 1) & 1);
+      if (q >= 1) {
+        const long long qq = q - 1;
+        const int buf = static_cast<int>(qq & 1);
+        mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < HALF / 16; ++j) {
@@ -587,20 +635,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        mbar_arrive_remote(&acc_empty[buf], 0);
+        __syncwarp();
+        if (lane == 0) arrive_leader(&acc_empty[buf], rank);
+        if (qq % nchunks == nchunks - 1) {  // tile complete: epilogue
+          long long m_pair;
+          int n_tile;
+          pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
+          const long long gm = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32 + lane;
+          float4* dst =
+              reinterpret_cast<float4*>(p.c + gm * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF);
+#pragma unroll
+          for (int i = 0; i < HALF / 4; ++i) {
+            const float4 v = make_float4(scalbnf(acc[4 * i], -shift), scalbnf(acc[4 * i + 1], -shift),
+                                         scalbnf(acc[4 * i + 2], -shift), scalbnf(acc[4 * i + 3], -shift));
+            local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
+            dst[i] = v;
+          }
+#pragma unroll
+          for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+        }
       }
     }
-    const long long gm = row0 + quad * 32 + lane;
-    const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
-    const int shift = sa + sb;
-    float local = 0.f;
-#pragma unroll
-    for (int i = 0; i < HALF; ++i) acc[i] = scalbnf(acc[i], -shift);
-#pragma unroll
-    for (int i = 0; i < HALF; i += 2) local = fmaxf(local, acc[i] * acc[i] + acc[i + 1] * acc[i + 1]);
-    float4* dst = reinterpret_cast<float4*>(p.c + gm * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF);
-#pragma unroll
-    for (int i = 0; i < HALF / 4; ++i) dst[i] = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
     if (p.meta_c) {
       for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
       if (lane == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
@@ -694,9 +749,25 @@ CUtensorMap make_map(const void* base, long long cols, long long rows, int box_r
   return m;
 }
 
+int chunk_blocks() {
+  const char* env = std::getenv("QSG_TC_CHUNK");
+  const int v = env ? std::atoi(env) : kChunkDefault;
+  return v >= 1 ? v : kChunkDefault;
+}
+
 bool raw_hi_mode() {
   const char* env = std::getenv("QSG_TC_RAWHI");
   return env && env[0] == '1';
+}
+
+// Persistent grid: one CTA pair per SM pair (74 on a 148-SM B200).
+long long pair_slots() {
+  static long long n = [] {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return static_cast<long long>(std::max(1, sms / 2));
+  }();
+  return n;
 }
 
 // The CTA-pair kernel covers 256 x 256 (real) tiles; QSG_TC_2SM=0 disables it.
@@ -770,6 +841,7 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     p.norm_a = g.norm_a;
     p.norm_b = g.norm_b;
     p.raw_hi = raw_hi_mode() ? 1 : 0;
+    p.chunk = chunk_blocks();
     const long long pairs = (g.m / 256) * ((2 * g.n) / kPairBN);
     if (2 * pairs > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
     p.n_tiles = static_cast<int>((2 * g.n) / kPairBN);
@@ -777,7 +849,8 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     std::call_once(once, [] {
       cudaFuncSetAttribute(cgemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg::SMEM);
     });
-    cgemm_tc2_kernel<<<static_cast<unsigned>(2 * pairs), kThreads, Tc2Cfg::SMEM, stream>>>(ma, mbh, mbl, p);
+    const long long clusters = std::min<long long>(pairs, pair_slots());
+    cgemm_tc2_kernel<<<static_cast<unsigned>(2 * clusters), kThreads, Tc2Cfg::SMEM, stream>>>(ma, mbh, mbl, p);
     if (launches) ++*launches;
     return cudaGetLastError();
   }
@@ -796,6 +869,7 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
   p.norm_a = g.norm_a;
   p.norm_b = g.norm_b;
   p.raw_hi = raw_hi_mode() ? 1 : 0;
+  p.chunk = chunk_blocks();
   const long long mt = g.m / BM, nt = (2 * g.n) / bn;
   if (mt * nt > 2147483647LL || g.m > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
   p.n_tiles = static_cast<int>(nt);
