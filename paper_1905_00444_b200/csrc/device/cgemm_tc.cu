@@ -805,8 +805,10 @@ bool cgemm_tc_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool tra
 
 bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
   if (!tc_enabled() || !cgemm_tc_supported(m, n, k, trans_a, trans_b)) return false;
-  // Worth it only for real work: >= ~1 GFLOP and a non-trivial K.
-  return 8.0 * static_cast<double>(m) * n * k >= 1e9 && k >= 64;
+  // Worth it for real work (>= ~1 GFLOP).  The persistent CTA-pair kernel
+  // streams even single-k-block tiles well; the 1-CTA kernel needs K >= 64.
+  if (8.0 * static_cast<double>(m) * n * k < 1e9) return false;
+  return use_pair(m, n) ? k >= 16 : k >= 64;
 }
 
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t /*m*/, std::int64_t n, std::int64_t k, bool, bool) {
