@@ -33,10 +33,18 @@ CONFIGS = {
           "workload": "config2: 7x7 RQC depth (1+32+1), reference 7x7 region order, 1 cut bond "
                       "b_007_003_004 (2 slices), 1024-amplitude batch per x1 draw",
           "slices_per_step": None},
+    "3": {"circuit": (6, 10, 32, 0), "plan": "configs/config3_standin_6x10_plan.json",
+          "workload": "config3 stand-in for Bristlecone-60: 6x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
+                      "(4096 slices), closed amplitude over a fixed 2^10-slice subset; 1 slice per step per GPU",
+          "slices_per_step": 1, "slices_per_batch": 1024},
+    "4": {"circuit": (7, 10, 32, 0), "plan": "configs/config4_standin_7x10_plan.json",
+          "workload": "config4 stand-in for Bristlecone-70: 7x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
+                      "(4096 slices), closed amplitude over a fixed 2^12-slice subset; 1 slice per step per GPU",
+          "slices_per_step": 1, "slices_per_batch": 4096},
     "5": {"circuit": (7, 7, 40, 0), "plan": "configs/config5_plan.json",
-          "workload": "config5: 7x7 RQC depth (1+40+1), reference_plan_7x7 (1024 slices), 64-amplitude batch, "
-                      "1 slice per step per GPU",
-          "slices_per_step": 1},
+          "workload": "config5: 7x7 RQC depth (1+40+1), reference_plan_7x7 (1024 slices), 64-amplitude batch at "
+                      "fidelity 6/1024 (6 slices per batch, as the paper's run); 1 slice per step per GPU",
+          "slices_per_step": 1, "slices_per_batch": 6},
 }
 
 
@@ -142,7 +150,7 @@ def run_reference_arm(args):
     nsteps = reference_prefix_steps(plan, args.cpu_budget_flops)
     prefix_flops = sum(s["flops"] for s in plan["steps"][:nsteps])
     batch = 1 << len(plan["open_qubits"])
-    slices_per_batch = cfg["slices_per_step"] or plan["slices"]
+    slices_per_batch = cfg.get("slices_per_batch") or plan["slices"]
     flops_per_step = plan["per_slice"]["flops"] * slices_per_batch
     for _ in range(args.warmup):
         cpu_reference_sample(cfg, nsteps, threads)
@@ -230,7 +238,9 @@ def run_ours(args):
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
-    amps_total = batch * args.steps * world
+    # batch mode: every step is a full amplitude batch; slice mode: a batch
+    # needs `slices_per_batch` slices (fidelity fraction / fixed subset).
+    amps_total = batch * args.steps * world * per_step / cfg.get("slices_per_batch", per_step)
     flops_total = info.flops_per_slice * per_step * args.steps * world
     value = amps_total / (ms / 1e3)
     tflops = flops_total / (ms / 1e3) / 1e12
@@ -321,7 +331,7 @@ def run_ours(args):
             nsteps = reference_prefix_steps(plan, args.cpu_budget_flops)
             secs, fl = cpu_reference_sample(cfg, nsteps, cpu_threads)
             rate = fl / secs
-            cpu_amps = rate / (info.flops_per_slice * per_step) * batch
+            cpu_amps = rate / (info.flops_per_slice * cfg.get("slices_per_batch", per_step)) * batch
             line["cpu_baseline"] = {
                 "value": cpu_amps, "unit": "amplitudes/s", "cores": cpu_threads, "kind": "reference",
                 "sample": f"unmodified reference kernels (oracle/_ref, Eigen->OpenBLAS 1-thread shim) over plan "
@@ -344,7 +354,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="2",
+                    help="BASELINE config: 1, 2 (default, the metric's workload), 3/4 (Bristlecone stand-ins), 5")
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)

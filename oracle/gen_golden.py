@@ -55,6 +55,24 @@ def config_plans():
     draft = {"version": 1, "open_qubits": open2, "cut": {"labels": ["b_007_003_004"], "group": 1}, "order": order}
     p2 = R.plan_json(c2, open2, R.PLAN_JSON, json.dumps(draft))
     out["config2"] = {"circuit": [7, 7, 32, 0], "plan": json.loads(p2)}
+    # Configs 3/4 (Bristlecone-60/70, depth 1+32+1): the reference defines no
+    # Bristlecone geometry, so the validated rectangular stand-ins of equal
+    # qubit count: 6x10 / 7x10, column-major sweep chained onto
+    # one accumulator, cut = the 4 bonds of the col-4|5 seam edge in rows
+    # 0, 1, 2 -> K = 4096 slices; closed plans (run_amplitudes path).
+    seam = ["b_001_004_005", "b_009_004_005", "b_017_004_005", "b_025_004_005",
+            "b_005_014_015", "b_013_014_015", "b_021_014_015", "b_029_014_015",
+            "b_001_024_025", "b_009_024_025", "b_017_024_025", "b_025_024_025"]
+    for rows, name in ((6, "config3_standin_6x10"), (7, "config4_standin_7x10")):
+        c = R.generate_rqc(rows, 10, 32, 0)
+        nodes = [r * 10 + col for col in range(10) for r in range(rows)]
+        order, acc = [], f"n_{nodes[0]:03d}"
+        for i, q in enumerate(nodes[1:]):
+            order.append([acc, f"n_{q:03d}"])
+            acc = f"s{i:03d}"
+        draft = {"version": 1, "open_qubits": [], "cut": {"labels": seam, "group": 1}, "order": order}
+        pj = R.plan_json(c, [], R.PLAN_JSON, json.dumps(draft))
+        out[name] = {"circuit": [rows, 10, 32, 0], "plan": json.loads(pj)}
     for name, d in out.items():
         with open(os.path.join(CONF, f"{name}_plan.json"), "w") as f:
             json.dump(d["plan"], f, indent=1)

@@ -380,15 +380,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // acc_empty[] live in the leader and collect arrivals from both CTAs'
 // workers (remote mbarrier arrive over the cluster); the leader's
 // tcgen05.commit multicasts to both CTAs.
-constexpr int kPairBN = 256;  // real output columns per CTA pair
+// Real output columns per CTA pair: 256 for wide GEMMs; 128/64/32 for the
+// narrow-N (GEMV-like, HBM-bound) contraction steps.
 constexpr int kGroupM = 8;    // m-pairs per rasterization group
+template <int BN>
 struct Tc2Cfg {
   static constexpr int A_B = BM * BK * 4;            // this CTA's 128 rows of A
-  static constexpr int B_B = (kPairBN / 2) * BK * 4; // this CTA's half of B_r^T
+  static constexpr int B_B = (BN / 2) * BK * 4;      // this CTA's half of B_r^T
   static constexpr int STAGE_BYTES = 2 * A_B + 2 * B_B;
-  static constexpr int STAGES = 3;
+  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 6 ? 6 : (200 * 1024 / STAGE_BYTES);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
-  static constexpr int TMEM_COLS = 2 * kPairBN;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // power of two >= 32
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -442,8 +444,9 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
       : "memory");
 }
 
+template <int BN>
 __host__ __device__ constexpr uint32_t tf32_idesc_pair() {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kPairBN >> 3) << 17) |
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
          (static_cast<uint32_t>(256 >> 4) << 24);
 }
 
@@ -465,10 +468,11 @@ __device__ __forceinline__ void pair_tile_coords(long long t, long long m_pairs,
 // with pipeline counters that run across tile boundaries, so TMA prefetch,
 // conversion and MMA of the next tile overlap the epilogue of the previous
 // one and the per-tile setup (barriers, TMEM allocation) is paid once.
+template <int kPairBN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cgemm_tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
                      const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
-  using Cfg = Tc2Cfg;
+  using Cfg = Tc2Cfg<kPairBN>;
   constexpr int HALF = kPairBN / 2;  // accumulator columns per worker thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -540,7 +544,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      constexpr uint32_t idesc = tf32_idesc_pair();
+      constexpr uint32_t idesc = tf32_idesc_pair<kPairBN>();
       long long g = 0;
       for (long long q = 0; q < total_chunks; ++q) {
         const int c = static_cast<int>(q % nchunks);
@@ -771,10 +775,44 @@ long long pair_slots() {
 }
 
 // The CTA-pair kernel covers 256 x 256 (real) tiles; QSG_TC_2SM=0 disables it.
+int pair_bn(std::int64_t n) {
+  for (int bn : {256, 128, 64, 32})
+    if ((2 * n) % bn == 0) return bn;
+  return 0;
+}
+
 bool use_pair(std::int64_t m, std::int64_t n) {
   const char* env = std::getenv("QSG_TC_2SM");
   if (env && env[0] == '0') return false;
-  return m % 256 == 0 && (2 * n) % kPairBN == 0;
+  return m % 256 == 0 && pair_bn(n) > 0;
+}
+
+template <int BN>
+cudaError_t launch_pair(const GemmArgs& g, const float* bhi, const float* blo, cudaStream_t stream) {
+  const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
+  const CUtensorMap mbh = make_map(bhi, 2 * g.k, 2 * g.n, BN / 2);
+  const CUtensorMap mbl = make_map(blo, 2 * g.k, 2 * g.n, BN / 2);
+  TcParams p{};
+  p.c = static_cast<float*>(g.c);
+  p.m = g.m;
+  p.n2 = 2 * g.n;
+  p.kblocks = static_cast<int>((2 * g.k) / BK);
+  p.meta_a = g.meta_a;
+  p.meta_b = g.meta_b;
+  p.meta_c = g.meta_c;
+  p.norm_a = g.norm_a;
+  p.norm_b = g.norm_b;
+  p.raw_hi = raw_hi_mode() ? 1 : 0;
+  p.chunk = chunk_blocks();
+  const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
+  p.n_tiles = static_cast<int>((2 * g.n) / BN);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(cgemm_tc2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg<BN>::SMEM);
+  });
+  const long long clusters = std::min<long long>(pairs, pair_slots());
+  cgemm_tc2_kernel<BN><<<static_cast<unsigned>(2 * clusters), kThreads, Tc2Cfg<BN>::SMEM, stream>>>(ma, mbh, mbl, p);
+  return cudaGetLastError();
 }
 
 int tc_bn(std::int64_t n) {
@@ -800,7 +838,8 @@ bool tc_enabled() {
 }
 
 bool cgemm_tc_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool /*trans_b*/) {
-  return !trans_a && m > 0 && m % BM == 0 && (2 * n) % 128 == 0 && n > 0 && (2 * k) % BK == 0 && k > 0;
+  if (trans_a || m <= 0 || n <= 0 || k <= 0 || (2 * k) % BK != 0) return false;
+  return (m % BM == 0 && (2 * n) % 128 == 0) || use_pair(m, n);
 }
 
 bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
@@ -829,32 +868,15 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     if (launches) ++*launches;
   }
   if (use_pair(g.m, g.n)) {
-    const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
-    const CUtensorMap mbh = make_map(bhi, 2 * g.k, 2 * g.n, kPairBN / 2);
-    const CUtensorMap mbl = make_map(blo, 2 * g.k, 2 * g.n, kPairBN / 2);
-    TcParams p{};
-    p.c = static_cast<float*>(g.c);
-    p.m = g.m;
-    p.n2 = 2 * g.n;
-    p.kblocks = static_cast<int>((2 * g.k) / BK);
-    p.meta_a = g.meta_a;
-    p.meta_b = g.meta_b;
-    p.meta_c = g.meta_c;
-    p.norm_a = g.norm_a;
-    p.norm_b = g.norm_b;
-    p.raw_hi = raw_hi_mode() ? 1 : 0;
-    p.chunk = chunk_blocks();
-    const long long pairs = (g.m / 256) * ((2 * g.n) / kPairBN);
-    if (2 * pairs > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
-    p.n_tiles = static_cast<int>((2 * g.n) / kPairBN);
-    static std::once_flag once;
-    std::call_once(once, [] {
-      cudaFuncSetAttribute(cgemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg::SMEM);
-    });
-    const long long clusters = std::min<long long>(pairs, pair_slots());
-    cgemm_tc2_kernel<<<static_cast<unsigned>(2 * clusters), kThreads, Tc2Cfg::SMEM, stream>>>(ma, mbh, mbl, p);
+    cudaError_t e = cudaSuccess;
+    switch (pair_bn(g.n)) {
+      case 256: e = launch_pair<256>(g, bhi, blo, stream); break;
+      case 128: e = launch_pair<128>(g, bhi, blo, stream); break;
+      case 64: e = launch_pair<64>(g, bhi, blo, stream); break;
+      default: e = launch_pair<32>(g, bhi, blo, stream); break;
+    }
     if (launches) ++*launches;
-    return cudaGetLastError();
+    return e;
   }
   const int bn = tc_bn(g.n);
   const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);

@@ -136,7 +136,9 @@ def test_cgemm_device_shapes_vs_fp64(gpu, m, n, k, ta, tb):
 
 
 @pytest.mark.parametrize("m,n,k,tb", [(128, 64, 16, 0), (256, 128, 64, 0), (1024, 256, 256, 0), (512, 192, 80, 1),
-                                      (4096, 128, 1024, 0), (1 << 15, 256, 256, 0)])
+                                      (4096, 128, 1024, 0), (1 << 15, 256, 256, 0),
+                                      # narrow-N CTA-pair variants (BN = 32 / 64 / 128 real columns)
+                                      (1 << 14, 16, 256, 0), (2048, 32, 64, 1), (1024, 64, 512, 0), (768, 48, 32, 0)])
 def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb):
     """tcgen05 3xTF32 path: FP32-level accuracy (1e-5 relative Frobenius, the
     reference's TTGT tolerance, test_tensor.cpp:120-155)."""
