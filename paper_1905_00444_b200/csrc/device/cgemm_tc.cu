@@ -388,8 +388,14 @@ struct Tc2Cfg {
   static constexpr int A_B = BM * BK * 4;            // this CTA's 128 rows of A
   static constexpr int B_B = (BN / 2) * BK * 4;      // this CTA's half of B_r^T
   static constexpr int STAGE_BYTES = 2 * A_B + 2 * B_B;
-  static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 6 ? 6 : (200 * 1024 / STAGE_BYTES);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  // Epilogue staging: per worker warp a 32-row x 16-float chunk, pitch 20
+  // floats (conflict-free 16-byte writes), so global stores are 64-byte row
+  // segments instead of one 16-byte piece of 32 different rows.
+  static constexpr int EPI_PITCH = 20;
+  static constexpr int EPI_BYTES = (kWorkers / 32) * 32 * EPI_PITCH * 4;
+  static constexpr int STAGES =
+      ((224 * 1024 - EPI_BYTES) / STAGE_BYTES) > 6 ? 6 : ((224 * 1024 - EPI_BYTES) / STAGE_BYTES);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // power of two >= 32
 };
 
@@ -482,6 +488,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = empty + Cfg::STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -645,15 +652,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           long long m_pair;
           int n_tile;
           pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
-          const long long gm = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32 + lane;
-          float4* dst =
-              reinterpret_cast<float4*>(p.c + gm * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF);
+          // Rows quad*32 .. +31 of this CTA, columns half*HALF .. +HALF.
+          const long long row_base = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32;
+          float* base = p.c + row_base * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF;
+          float* stg = epi_stage + (warp - 2) * 32 * Cfg::EPI_PITCH;
 #pragma unroll
-          for (int i = 0; i < HALF / 4; ++i) {
-            const float4 v = make_float4(scalbnf(acc[4 * i], -shift), scalbnf(acc[4 * i + 1], -shift),
-                                         scalbnf(acc[4 * i + 2], -shift), scalbnf(acc[4 * i + 3], -shift));
-            local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
-            dst[i] = v;
+          for (int c0 = 0; c0 < HALF; c0 += 16) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 v = make_float4(scalbnf(acc[c0 + 4 * i], -shift), scalbnf(acc[c0 + 4 * i + 1], -shift),
+                                           scalbnf(acc[c0 + 4 * i + 2], -shift), scalbnf(acc[c0 + 4 * i + 3], -shift));
+              local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
+              *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int r = it * 8 + (lane >> 2), c4 = lane & 3;
+              const float4 v = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 4 * c4);
+              *reinterpret_cast<float4*>(base + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) = v;
+            }
+            __syncwarp();
           }
 #pragma unroll
           for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
