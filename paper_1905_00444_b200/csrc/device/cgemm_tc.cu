@@ -91,6 +91,9 @@ struct TcParams {
   TMeta* meta_c;
   int norm_a, norm_b;
   int chunk;   // k-blocks per TMEM promotion chunk
+  int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
+  unsigned char row_pos[48];
+  unsigned char col_pos[24];
   int raw_hi;  // experiment: feed raw fp32 as the hi part (valid iff the tensor core truncates)
 };
 
@@ -656,6 +659,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const long long row_base = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32;
           float* base = p.c + row_base * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF;
           float* stg = epi_stage + (warp - 2) * 32 * Cfg::EPI_PITCH;
+          // Fused output permutation: complex offset of (own row, tile's first column).
+          long long my_row_off = 0, col_tile_off = 0;
+          if (p.store_perm) {
+            const long long grow = row_base + lane;
+            for (int b = 0; b < p.nrow_bits; ++b)
+              if ((grow >> b) & 1) my_row_off += 1ll << p.row_pos[b];
+            const long long gcol = (static_cast<long long>(n_tile) * kPairBN + half * HALF) / 2;
+            for (int b = 0; b < p.ncol_bits; ++b)
+              if ((gcol >> b) & 1) col_tile_off += 1ll << p.col_pos[b];
+          }
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += 16) {
 #pragma unroll
@@ -666,11 +679,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
             }
             __syncwarp();
+            long long jc_off = 0;  // complex column offset of this lane's float4 within the chunk
+            if (p.store_perm) {
+              const int jloc = (c0 >> 1) + 2 * (lane & 3);  // complex column within the tile half
+              for (int b = 0; b < 7 && b < p.ncol_bits; ++b)
+                if ((jloc >> b) & 1) jc_off += 1ll << p.col_pos[b];
+            }
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
               const int r = it * 8 + (lane >> 2), c4 = lane & 3;
               const float4 v = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 4 * c4);
-              *reinterpret_cast<float4*>(base + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) = v;
+              if (p.store_perm) {
+                const long long ro = __shfl_sync(0xffffffffu, my_row_off, r);
+                *reinterpret_cast<float4*>(p.c + 2 * (ro + col_tile_off + jc_off)) = v;
+              } else {
+                *reinterpret_cast<float4*>(base + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) = v;
+              }
             }
             __syncwarp();
           }
@@ -823,6 +847,11 @@ cudaError_t launch_pair(const GemmArgs& g, const float* bhi, const float* blo, c
   p.norm_b = g.norm_b;
   p.raw_hi = raw_hi_mode() ? 1 : 0;
   p.chunk = chunk_blocks();
+  p.store_perm = g.store_perm ? 1 : 0;
+  p.nrow_bits = g.nrow_bits;
+  p.ncol_bits = g.ncol_bits;
+  std::memcpy(p.row_pos, g.row_pos, sizeof p.row_pos);
+  std::memcpy(p.col_pos, g.col_pos, sizeof p.col_pos);
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
   static std::once_flag once;
@@ -865,8 +894,14 @@ bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool tran
   if (!tc_enabled() || !cgemm_tc_supported(m, n, k, trans_a, trans_b)) return false;
   // Worth it for real work (>= ~1 GFLOP).  The persistent CTA-pair kernel
   // streams even single-k-block tiles well; the 1-CTA kernel needs K >= 64.
-  if (8.0 * static_cast<double>(m) * n * k < 1e9) return false;
+  const char* env = std::getenv("QSG_TC_MIN_FLOPS");  // tests force small shapes onto the TC path
+  const double min_flops = env ? std::atof(env) : 1e9;
+  if (8.0 * static_cast<double>(m) * n * k < min_flops) return false;
   return use_pair(m, n) ? k >= 16 : k >= 64;
+}
+
+bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
+  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n);
 }
 
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t /*m*/, std::int64_t n, std::int64_t k, bool, bool) {
@@ -886,6 +921,8 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
                                                 raw_hi_mode() ? 1 : 0);
     if (launches) ++*launches;
   }
+  if (g.store_perm && !use_pair(g.m, g.n))
+    throw std::invalid_argument("cgemm_tc: fused output permutation needs the CTA-pair path");
   if (use_pair(g.m, g.n)) {
     cudaError_t e = cudaSuccess;
     switch (pair_bn(g.n)) {

@@ -51,6 +51,15 @@ struct GemmArgs {
   TMeta* meta_c;
   void* workspace;
   std::int64_t workspace_bytes;
+  // Optional fused output permutation (tcgen05 CTA-pair path only): C is
+  // stored at complex offset sum_b bit_b(row) << row_pos[b] +
+  // sum_b bit_b(col) << col_pos[b] instead of row * n + col, i.e. directly in
+  // the layout the consuming step wants.  row/col bit b = LSB-first bits of
+  // the row (m) / complex column (n) index.  Requires col_pos[0..2] = 0,1,2.
+  bool store_perm = false;
+  int nrow_bits = 0, ncol_bits = 0;
+  unsigned char row_pos[48] = {};
+  unsigned char col_pos[24] = {};
 };
 std::int64_t cgemm_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
 cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);

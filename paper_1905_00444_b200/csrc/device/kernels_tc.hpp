@@ -14,6 +14,8 @@ namespace qsg::dev {
 bool cgemm_tc_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 // Supported and worth it (the engine uses this).
 bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
+// The fused output permutation is available (CTA-pair kernel path).
+bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
 // Process-wide switch (QSG_TENSOR_CORES=0 disables); the engine also has

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <set>
 #include <numeric>
 #include <sstream>
 #include <stdexcept>
@@ -275,6 +276,31 @@ void Engine::compile() {
           if (c.cost < best.cost) best = c;
         }
 
+    // Lookahead: the labels the consuming step will contract this output
+    // against (its other operand's label set).
+    std::set<Label> next_con;
+    bool has_next = false;
+    for (std::size_t sj = si + 1; sj < plan_.steps.size() && !has_next; ++sj) {
+      const auto& nx = plan_.steps[sj];
+      if (nx.lhs != step.out && nx.rhs != step.out) continue;
+      const std::string& other = nx.lhs == step.out ? nx.rhs : nx.lhs;
+      auto lv = live.find(other);
+      if (lv != live.end()) {
+        next_con.insert(lv->second.labels.begin(), lv->second.labels.end());
+      } else {
+        for (std::size_t sk = 0; sk < sj; ++sk)
+          if (plan_.steps[sk].out == other)
+            next_con.insert(plan_.steps[sk].out_labels.begin(), plan_.steps[sk].out_labels.end());
+      }
+      has_next = true;
+    }
+    // Free labels the next step contracts go last (they become the
+    // trailing bits of the output, so it is usable there without a permute).
+    auto next_last = [&](std::vector<Label> v) {
+      std::stable_partition(v.begin(), v.end(), [&](const Label& l) { return next_con.count(l) == 0; });
+      return v;
+    };
+
     const View& X = best.swap ? R : L;
     const View& Y = best.swap ? L : R;
     std::vector<Label> xfree, yfree;
@@ -282,6 +308,8 @@ void Engine::compile() {
       if (!Y.has(l)) xfree.push_back(l);
     for (const auto& l : Y.labels)
       if (!X.has(l)) yfree.push_back(l);
+    xfree = next_last(xfree);
+    yfree = next_last(yfree);
     View A = X, B = Y;
     if (!best.use_a) {
       std::vector<Label> order = xfree;
@@ -323,14 +351,45 @@ void Engine::compile() {
     touch(B.buf);
     g.c = new_buf(g.m * g.n * 8);
     if (g.ws_bytes > 0) g.ws = new_buf(g.ws_bytes);
+
+    // Output layout.  Natural GEMM order is [a_free, b_free]; when the
+    // tcgen05 pair kernel runs, the epilogue can scatter C straight into
+    // [free_next..., a_free ∩ con_next, b_free ∩ con_next] -- the layout the
+    // consuming step uses in place -- provided the three lowest column bits
+    // stay the three lowest output bits (64-byte store runs).
+    std::vector<Label> out_order = a_free;
+    out_order.insert(out_order.end(), b_free.begin(), b_free.end());
+    if (has_next && g.tc && dev::cgemm_tc_store_perm_supported(g.m, g.n, k, g.ta, g.tb) && a_free.size() <= 48 &&
+        b_free.size() <= 24 && b_free.size() >= 3) {
+      std::vector<Label> fr, cn;
+      for (const auto& l : a_free) (next_con.count(l) ? cn : fr).push_back(l);
+      std::vector<Label> cn_b;
+      for (const auto& l : b_free) (next_con.count(l) ? cn_b : fr).push_back(l);
+      std::vector<Label> cand = fr;
+      cand.insert(cand.end(), cn.begin(), cn.end());
+      cand.insert(cand.end(), cn_b.begin(), cn_b.end());
+      bool ok = cand != out_order;
+      for (const auto& l : cand) ok = ok && (A.has(l) ? A.dim_of(l) : B.dim_of(l)) == 2;
+      for (std::size_t t = 1; t <= 3 && ok; ++t) ok = cand[cand.size() - t] == b_free[b_free.size() - t];
+      if (ok) {
+        auto pos = [&](const Label& l) {
+          return static_cast<unsigned char>(cand.size() - 1 - (std::find(cand.begin(), cand.end(), l) - cand.begin()));
+        };
+        g.store_perm = true;
+        g.nrow_bits = static_cast<int>(a_free.size());
+        g.ncol_bits = static_cast<int>(b_free.size());
+        for (std::size_t b = 0; b < a_free.size(); ++b) g.row_pos[b] = pos(a_free[a_free.size() - 1 - b]);
+        for (std::size_t b = 0; b < b_free.size(); ++b) g.col_pos[b] = pos(b_free[b_free.size() - 1 - b]);
+        out_order = cand;
+      }
+    }
     ops_.push_back(g);
 
     View C;
     C.buf = g.c;
     C.off = 0;
     C.meta = static_cast<int>(si);
-    C.labels = a_free;
-    C.labels.insert(C.labels.end(), b_free.begin(), b_free.end());
+    C.labels = out_order;
     for (const auto& l : C.labels) C.dims.push_back(A.has(l) ? A.dim_of(l) : B.dim_of(l));
     C.strides = row_major_strides(C.dims);
     live[step.out] = std::move(C);
@@ -454,6 +513,11 @@ void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off,
     g.meta_c = metas_ + op.meta_c;
     g.workspace = op.ws >= 0 ? arena_ + bufs_[static_cast<std::size_t>(op.ws)].offset : nullptr;
     g.workspace_bytes = op.ws_bytes;
+    g.store_perm = op.store_perm;
+    g.nrow_bits = op.nrow_bits;
+    g.ncol_bits = op.ncol_bits;
+    std::copy(op.row_pos.begin(), op.row_pos.end(), g.row_pos);
+    std::copy(op.col_pos.begin(), op.col_pos.end(), g.col_pos);
     if (op.tc) check(dev::cgemm_tc(g, stream_, &launches), "cgemm_tc");
     else check(dev::cgemm(g, stream_, &launches), "cgemm");
   } else {
@@ -563,7 +627,8 @@ std::string Engine::describe() const {
     if (op.kind == 0) os << "  permute step " << op.step << " elems " << op.count << " rank " << op.ext.size() << "\n";
     else if (op.kind == 1)
       os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << " flops " << op.flops
-         << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes << "\n";
+         << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes
+         << (op.store_perm ? " fused-store" : "") << "\n";
     else os << "  accumulate " << op.count << "\n";
   }
   return os.str();

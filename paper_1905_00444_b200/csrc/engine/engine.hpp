@@ -20,6 +20,7 @@
 // Slices run back to back on one stream; K3 accumulates them in order.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -115,6 +116,10 @@ class Engine {
     bool tc = false;
     std::int64_t count = 0;  // accumulate / permute elements
     std::uint64_t flops = 0;
+    bool store_perm = false;  // fused output permutation (see dev::GemmArgs)
+    int nrow_bits = 0, ncol_bits = 0;
+    std::array<unsigned char, 48> row_pos{};
+    std::array<unsigned char, 24> col_pos{};
   };
 
   void compile();

@@ -169,3 +169,28 @@ def test_config2_full_size_tensor_core_vs_simt(gpu):
     assert fid >= 1 - 1e-6
     # Porter-Thomas: E[2^n |a|^2] = 1 over random bitstrings (loose, 1024 samples)
     assert 0.8 < np.mean(np.abs(a) ** 2) * 2.0**49 < 1.25
+
+
+def test_tensor_core_paths_forced_small_vs_oracle(gpu, monkeypatch):
+    """Forces every supported GEMM onto the tcgen05 path (QSG_TC_MIN_FLOPS=0)
+    on a 7x7 (1+20+1) circuit with the config-2 region order and cut, so the
+    CTA-pair kernel, its narrow-N variants and the fused output permutation
+    (lookahead layouts) all run at a size the numpy oracle checks exactly."""
+    import qsim_oracle as O
+    monkeypatch.setenv("QSG_TC_MIN_FLOPS", "0")
+    text = gpu.generate_rqc(7, 7, 20, 0)
+    order = json.load(open(os.path.join(ROOT, "configs", "config2_plan.json")))["order"]
+    opn = [32, 33, 34, 39, 40, 41, 45, 46, 47, 48]
+    plan = json.dumps({"version": 1, "open_qubits": opn, "cut": {"labels": ["b_007_003_004"], "group": 1},
+                       "order": order})
+    listing = gpu.program_listing(text, plan)
+    assert "fused-store" in listing and " tc " in listing
+    x1 = gpu.draw_x1(49, opn, 3, 0)
+    with gpu.Engine(text, plan) as e:
+        bits, amps = e.amplitude_batch(x1, [0, 1])
+    obits, oamps = O.amplitude_batch(text, plan, x1, [0, 1])
+    assert bits == obits
+    assert rel(amps, oamps) < 1e-5
+    with gpu.Engine(text, plan, tensor_cores=False) as e:
+        _, samps = e.amplitude_batch(x1, [0, 1])
+    assert rel(amps, samps) < 1e-5
