@@ -205,6 +205,36 @@ int qsg_amplitude_batch(qsg_engine* e, const int* x1_bits, int n, const int64_t*
 int qsg_run_amplitudes(qsg_engine* e, const char* bitstrings, int nb, int n, int64_t frac_num, int64_t frac_den,
                        uint64_t seed, double* out, int64_t* ids_out, uint64_t* flops);
 
+/* ---------------------------------------------------------------------------
+ * Sampling and XEB on device amplitude batches (SURVEY 8f "next")
+ * ------------------------------------------------------------------------- */
+
+typedef struct qsg_sample_stats {
+  uint64_t x1_draws, redraws, cap_hits, candidates;
+  int64_t exact_count, uniform_count;
+} qsg_sample_stats;
+
+typedef struct qsg_xeb_report {
+  int32_t n, hog_available;
+  int64_t size, zero_excluded;
+  double mean_log_prob, cross_entropy, fidelity_estimate, hog_fraction;
+} qsg_xeb_report;
+
+/* sample() (src/sampler.cpp:122-178; amplitude_fraction_mode = 1 is
+ * sample_amplitude_fraction, :180-185): frugal rejection sampling with x1/x2
+ * recycling over the engine's open qubits.  Fraction frac_num/frac_den
+ * (den <= 0: all slices), rejection cap kappa, seed.  Outputs: M bitstrings
+ * of n chars (concatenated), M probabilities (-1 = uniform share), stats,
+ * and the self-XEB of the emitted probabilities. */
+int qsg_sample(qsg_engine* e, int64_t num_samples, int64_t frac_num, int64_t frac_den, int amplitude_fraction_mode,
+               double rejection_cap, uint64_t seed, char* bitstrings_out, double* probs_out, qsg_sample_stats* stats,
+               qsg_xeb_report* self_xeb);
+
+/* xeb_score (src/sampler.cpp:187-215): cross entropy -<log p>, fidelity
+ * 2^n <p> - 1 over p > 0 (zeros excluded and counted), HOG fraction above
+ * `hog_median` when has_median != 0. */
+int qsg_xeb_score(int n, const double* probs, int64_t count, int has_median, double hog_median, qsg_xeb_report* out);
+
 #ifdef __cplusplus
 }
 #endif

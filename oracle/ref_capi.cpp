@@ -29,6 +29,8 @@
 #include "qsim/tensor.hpp"
 #include "qsim/tensor_io.hpp"
 
+#include <nlohmann/json.hpp>
+
 extern "C" void scipy_openblas_set_num_threads64_(int);
 
 using namespace qsim;
@@ -283,6 +285,32 @@ int ref_execute_prefix(const char* text, const char* plan_text, int plan_kind, c
     });
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *flops = counter.total();
+  });
+}
+
+// sample() (src/sampler.cpp:122-178) on a plan with open qubits; bitstrings
+// (M * n chars) and probabilities out.
+int ref_sample(const char* text, const char* plan_text, std::int64_t num_samples, std::int64_t frac_num,
+               std::int64_t frac_den, int amplitude_mode, double cap, std::uint64_t seed, char* bits_out,
+               double* probs_out) {
+  return guarded([&] {
+    Circuit c = parse_circuit(std::string(text));
+    // The plan JSON carries its open qubits.
+    auto j = nlohmann::json::parse(plan_text);
+    std::vector<int> open = j.at("open_qubits").get<std::vector<int>>();
+    ContractionPlan plan = plan_from_json(plan_text, fold_shape(c, open));
+    SamplingConfig cfg;
+    cfg.num_samples = static_cast<std::size_t>(num_samples);
+    cfg.fraction = frac_den > 0 ? Fraction{frac_num, frac_den} : Fraction{plan.num_slices, plan.num_slices};
+    cfg.mode = amplitude_mode ? FidelityMode::amplitude_fraction : FidelityMode::path_fraction;
+    cfg.rejection_cap = cap;
+    cfg.seed = seed;
+    auto out = sample(c, plan, cfg);
+    const int n = c.num_qubits();
+    for (std::size_t i = 0; i < out.bitstrings.size(); ++i) {
+      std::memcpy(bits_out + i * static_cast<std::size_t>(n), out.bitstrings[i].data(), static_cast<std::size_t>(n));
+      probs_out[i] = out.probabilities[i];
+    }
   });
 }
 

@@ -51,6 +51,9 @@ def lib():
                                         i32, P(i32), P(C.c_float), P(C.c_double), P(u64), i32]
         L.ref_execute_prefix.argtypes = [C.c_char_p, C.c_char_p, i32, P(i32), i32, i32, i32, i32, u64,
                                          P(C.c_double), P(u64)]
+        L.ref_sample.argtypes = [C.c_char_p, C.c_char_p, i64, i64, i64, i32, C.c_double, u64, C.c_char_p,
+                                 P(C.c_double)]
+        L.ref_sample.restype = i32
         for name in ("ref_generate_rqc", "ref_canonical_circuit", "ref_evolve", "ref_plan_json",
                      "ref_fold_qtns", "ref_select_slices", "ref_amplitude_batch", "ref_run_amplitudes",
                      "ref_transpose", "ref_contract_step", "ref_execute_prefix"):
@@ -226,3 +229,14 @@ def execute_prefix(text: str, plan_text: str, open_qubits, nsteps: int, ntasks: 
     _check(lib().ref_execute_prefix(text.encode(), plan_text.encode(), kind, p, len(a), nsteps, ntasks, threads,
                                     seed, C.byref(sec), C.byref(fl)))
     return sec.value, int(fl.value)
+
+
+def sample(text: str, plan_text: str, num_samples: int, frac=(0, 0), amplitude_mode=False, cap=6.0, seed=0):
+    """The reference sample() (src/sampler.cpp:122-178): (bitstrings, probabilities)."""
+    n = int(text.split("\n", 1)[0])
+    bits = C.create_string_buffer(num_samples * n)
+    probs = np.zeros(num_samples, dtype=np.float64)
+    _check(lib().ref_sample(text.encode(), plan_text.encode(), num_samples, frac[0], frac[1],
+                            1 if amplitude_mode else 0, cap, seed, bits, _ptr(probs, C.c_double)))
+    raw = bits.raw
+    return [raw[i * n:(i + 1) * n].decode() for i in range(num_samples)], probs

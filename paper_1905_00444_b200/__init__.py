@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libqsg.so")
 
 __all__ = [
     "QsgError", "CircuitError", "lib", "mix_seed", "flop_count", "generate_rqc", "canonical_circuit",
-    "circuit_info", "plan_json", "fold_worldlines", "select_slices", "draw_x1", "transpose", "contract", "normalize_inplace",
+    "circuit_info", "plan_json", "fold_worldlines", "select_slices", "draw_x1", "xeb_score", "transpose", "contract", "normalize_inplace",
     "Engine", "PLAN_JSON", "PLAN_REF7X7", "PLAN_GREEDY", "device_count",
 ]
 
@@ -69,6 +69,21 @@ class _EngineInfo(C.Structure):
                 ("num_steps", C.c_int64), ("max_rank", C.c_int64), ("peak_memory", C.c_int64),
                 ("arena_bytes", C.c_int64), ("node_bytes", C.c_int64), ("flops_per_slice", C.c_uint64),
                 ("num_ops", C.c_int64)]
+
+
+class _SampleStats(C.Structure):
+    _fields_ = [("x1_draws", C.c_uint64), ("redraws", C.c_uint64), ("cap_hits", C.c_uint64),
+                ("candidates", C.c_uint64), ("exact_count", C.c_int64), ("uniform_count", C.c_int64)]
+
+
+class _XebReport(C.Structure):
+    _fields_ = [("n", C.c_int32), ("hog_available", C.c_int32), ("size", C.c_int64), ("zero_excluded", C.c_int64),
+                ("mean_log_prob", C.c_double), ("cross_entropy", C.c_double), ("fidelity_estimate", C.c_double),
+                ("hog_fraction", C.c_double)]
+
+
+def _struct_dict(s):
+    return {f[0]: getattr(s, f[0]) for f in s._fields_}
 
 
 _lib = None
@@ -123,6 +138,8 @@ def lib():
         "qsg_engine_set_profile": (i32, [vp, i32]),
         "qsg_amplitude_batch": (i32, [vp, P(i32), i32, P(i64), i64, dp, cp]),
         "qsg_run_amplitudes": (i32, [vp, cp, i32, i32, i64, i64, u64, dp, P(i64), P(u64)]),
+        "qsg_sample": (i32, [vp, i64, i64, i64, i32, C.c_double, u64, cp, dp, P(_SampleStats), P(_XebReport)]),
+        "qsg_xeb_score": (i32, [i32, dp, i64, i32, C.c_double, P(_XebReport)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -324,6 +341,15 @@ def program_listing(circuit_text: str, plan_text: str = "", kind: int = PLAN_JSO
                  0 if tensor_cores else 2)
 
 
+def xeb_score(n: int, probs, hog_median=None) -> dict:
+    """xeb_score (src/sampler.cpp:187-215): cross entropy, 2^n<p>-1 fidelity, HOG fraction."""
+    a = np.ascontiguousarray(np.asarray(probs, dtype=np.float64))
+    r = _XebReport()
+    _check(lib().qsg_xeb_score(n, _p(a, C.c_double), len(a), 0 if hog_median is None else 1,
+                               0.0 if hog_median is None else float(hog_median), C.byref(r)))
+    return _struct_dict(r)
+
+
 # ---- engine ---------------------------------------------------------------
 
 @dataclass
@@ -447,6 +473,20 @@ class Engine:
         raw = bits.raw
         n = len(a)
         return [raw[i * n:(i + 1) * n].decode() for i in range(self.info.batch_size)], amps.view(np.complex128)
+
+    def sample(self, num_samples: int, fraction=(0, 0), amplitude_fraction: bool = False, cap: float = 6.0,
+               seed: int = 0):
+        """sample / sample_amplitude_fraction (src/sampler.cpp:122-185):
+        (bitstrings, probabilities, stats, self_xeb)."""
+        n = self.n
+        bits = C.create_string_buffer(max(1, num_samples * n))
+        probs = np.zeros(max(1, num_samples), dtype=np.float64)
+        st, xr = _SampleStats(), _XebReport()
+        _check(lib().qsg_sample(self._h, num_samples, fraction[0], fraction[1], 1 if amplitude_fraction else 0, cap,
+                                seed, bits, _p(probs, C.c_double), C.byref(st), C.byref(xr)))
+        raw = bits.raw
+        return ([raw[i * n:(i + 1) * n].decode() for i in range(num_samples)], probs[:num_samples],
+                _struct_dict(st), _struct_dict(xr))
 
     def run_amplitudes(self, bitstrings, fraction=(0, 0), seed: int = 0):
         """run_amplitudes (src/engine.cpp:300-378): (amplitudes, slice_ids, flops)."""

@@ -17,6 +17,7 @@
 #include "device/kernels.hpp"
 #include "device/kernels_tc.hpp"
 #include "engine/engine.hpp"
+#include "engine/sampler.hpp"
 #include "host/qsg_host.hpp"
 
 struct qsg_engine {
@@ -569,6 +570,59 @@ int qsg_run_amplitudes(qsg_engine* e, const char* bitstrings, int nb, int n, int
     }
     if (ids_out) std::copy(res.slice_ids.begin(), res.slice_ids.end(), ids_out);
     if (flops) *flops = res.total_flops;
+  });
+}
+
+namespace {
+qsg_xeb_report to_c(const qsg::XebReport& r) {
+  qsg_xeb_report o{};
+  o.n = r.n;
+  o.hog_available = r.hog_available ? 1 : 0;
+  o.size = static_cast<int64_t>(r.size);
+  o.zero_excluded = static_cast<int64_t>(r.zero_excluded);
+  o.mean_log_prob = r.mean_log_prob;
+  o.cross_entropy = r.cross_entropy;
+  o.fidelity_estimate = r.fidelity_estimate;
+  o.hog_fraction = r.hog_fraction;
+  return o;
+}
+}  // namespace
+
+int qsg_sample(qsg_engine* e, int64_t num_samples, int64_t frac_num, int64_t frac_den, int amplitude_fraction_mode,
+               double rejection_cap, uint64_t seed, char* bitstrings_out, double* probs_out, qsg_sample_stats* stats,
+               qsg_xeb_report* self_xeb) {
+  return guarded([&] {
+    qsg::SamplingConfig cfg;
+    cfg.num_samples = static_cast<std::size_t>(num_samples);
+    const auto K = e->impl->plan().num_slices;
+    cfg.fraction = frac_den > 0 ? qsg::Fraction{frac_num, frac_den} : qsg::Fraction{K, K};
+    if (cfg.fraction.den < 1 || cfg.fraction.num < 1 || cfg.fraction.num > cfg.fraction.den)
+      throw std::invalid_argument("fraction out of range");
+    cfg.amplitude_fraction_mode = amplitude_fraction_mode != 0;
+    cfg.rejection_cap = rejection_cap;
+    cfg.seed = seed;
+    const auto out = qsg::sample(*e->impl, cfg);
+    const int n = e->impl->circuit().num_qubits();
+    for (std::size_t i = 0; i < out.bitstrings.size(); ++i) {
+      if (bitstrings_out) std::memcpy(bitstrings_out + i * static_cast<std::size_t>(n), out.bitstrings[i].data(), static_cast<std::size_t>(n));
+      if (probs_out) probs_out[i] = out.probabilities[i];
+    }
+    if (stats) {
+      stats->x1_draws = out.stats.x1_draws;
+      stats->redraws = out.stats.redraws;
+      stats->cap_hits = out.stats.cap_hits;
+      stats->candidates = out.stats.candidates;
+      stats->exact_count = static_cast<int64_t>(out.stats.exact_count);
+      stats->uniform_count = static_cast<int64_t>(out.stats.uniform_count);
+    }
+    if (self_xeb) *self_xeb = to_c(out.self_xeb);
+  });
+}
+
+int qsg_xeb_score(int n, const double* probs, int64_t count, int has_median, double hog_median, qsg_xeb_report* out) {
+  return guarded([&] {
+    const std::vector<double> p(probs, probs + count);
+    *out = to_c(qsg::xeb_score(n, p, has_median ? &hog_median : nullptr));
   });
 }
 
