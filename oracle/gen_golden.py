@@ -230,6 +230,19 @@ def main():
     np.savez_compressed(os.path.join(GOLD, "amplitudes.npz"), **am)
     with open(os.path.join(GOLD, "amplitudes.json"), "w") as f:
         json.dump({"cases": meta, "config1": cfg1}, f, indent=1)
+    # 8. sampling: the reference sample() (src/sampler.cpp:122-178) on a 4x4
+    #    (1+12+1) circuit, x2 = qubits 10..15 (64-amplitude batches), full
+    #    fidelity and a 2-slice cut plan at path fraction 1/2.
+    t = R.generate_rqc(4, 4, 12, 0)
+    p_full = R.plan_json(t, list(range(10, 16)), R.PLAN_GREEDY)
+    p_cut = R.plan_json(t, list(range(10, 16)), R.PLAN_GREEDY, "", 8192)  # one cut bond -> 2 slices
+    samp = {"circuit": [4, 4, 12, 0], "plan_full": p_full, "plan_cut": p_cut, "runs": []}
+    for plan_text, frac, amode in ((p_full, (0, 0), False), (p_cut, (1, 2), False), (p_cut, (1, 2), True)):
+        bits, probs = R.sample(t, plan_text, 200, frac, amode, 6.0, 7)
+        samp["runs"].append({"plan": "full" if plan_text == p_full else "cut", "frac": list(frac),
+                             "amplitude_mode": amode, "seed": 7, "bitstrings": bits, "probs": probs.tolist()})
+    with open(os.path.join(GOLD, "sampling.json"), "w") as f:
+        json.dump(samp, f)
     print("golden fixtures written to", GOLD)
 
 

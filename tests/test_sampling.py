@@ -1,0 +1,78 @@
+"""Sampling + XEB on device amplitude batches (reference src/sampler.cpp,
+SPEC acceptance #4-#6).
+
+CPU: xeb_score formula (SPEC #6: uniform probabilities -> cross entropy
+n*log 2 exactly, fidelity 0; zero probabilities excluded and counted; HOG).
+GPU: the engine's sampler reproduces the reference sample() draw for draw
+(same RNG streams; committed golden from the unmodified reference), and the
+XEB fidelity of its samples, scored with the exact state vector, tracks the
+path / amplitude fraction (SPEC #4, #5)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1905_00444_b200 as Q
+from conftest import GOLDEN
+
+
+def test_xeb_score_uniform_and_edge_cases():
+    n = 12
+    r = Q.xeb_score(n, [2.0 ** -n] * 1000)
+    assert r["cross_entropy"] == pytest.approx(n * math.log(2), rel=0, abs=1e-12)
+    assert abs(r["fidelity_estimate"]) < 1e-12
+    r = Q.xeb_score(3, [0.0, 0.25, 0.125], hog_median=0.2)
+    assert r["zero_excluded"] == 1 and r["size"] == 2
+    assert r["fidelity_estimate"] == pytest.approx(8 * (0.375 / 2) - 1)
+    assert r["hog_available"] == 1 and r["hog_fraction"] == pytest.approx(0.5)
+    r = Q.xeb_score(4, [])
+    assert r["size"] == 0
+
+
+def _golden():
+    return json.load(open(os.path.join(GOLDEN, "sampling.json")))
+
+
+@pytest.mark.gpu
+def test_sampler_matches_reference_draw_for_draw(gpu):
+    g = _golden()
+    r, c, m, s = g["circuit"]
+    text = gpu.generate_rqc(r, c, m, s)
+    for run in g["runs"]:
+        plan = g["plan_full"] if run["plan"] == "full" else g["plan_cut"]
+        with gpu.Engine(text, plan) as e:
+            bits, probs, stats, xeb = e.sample(len(run["bitstrings"]), tuple(run["frac"]), run["amplitude_mode"],
+                                               6.0, run["seed"])
+        same = [a == b for a, b in zip(bits, run["bitstrings"])]
+        # identical RNG streams: only an FP32-level amplitude difference at an
+        # accept threshold could flip a draw
+        assert sum(same) >= 0.97 * len(same), sum(same)
+        for ok, p, q in zip(same, probs, run["probs"]):
+            if ok and q >= 0:
+                assert p == pytest.approx(q, rel=1e-4)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("plan_key,frac,amode,want", [("plan_full", (0, 0), False, 1.0),
+                                                      ("plan_cut", (1, 2), False, 0.5),
+                                                      ("plan_cut", (1, 2), True, 0.5)])
+def test_xeb_fidelity_tracks_fraction(gpu, plan_key, frac, amode, want):
+    import qsim_oracle as O
+    g = _golden()
+    r, c, m, s = g["circuit"]
+    text = gpu.generate_rqc(r, c, m, s)
+    sv = O.evolve(text)
+    M = 4000
+    with gpu.Engine(text, g[plan_key]) as e:
+        bits, probs, stats, _ = e.sample(M, frac, amode, 6.0, 11)
+    p_ideal = np.abs(sv[[int(b, 2) for b in bits]]) ** 2
+    rep = gpu.xeb_score(16, p_ideal)
+    assert abs(rep["fidelity_estimate"] - want) < 0.12, rep
+    if amode:
+        assert stats["exact_count"] == M // 2 and stats["uniform_count"] == M - M // 2
+    # determinism (worker/seed contract): same seed -> same samples
+    with gpu.Engine(text, g[plan_key]) as e:
+        bits2, _, _, _ = e.sample(50, frac, amode, 6.0, 11)
+    assert bits2 == bits[:50]
