@@ -504,12 +504,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < Cfg::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 2 * kWorkers / 32);  // one arrival per worker warp of each CTA
+      mbar_init(&conv[s], 2);  // one (aggregated) arrival per CTA
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
-      mbar_init(&acc_empty[b], 2 * kWorkers / 32);
+      mbar_init(&acc_empty[b], 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -533,29 +533,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      long long g = 0;  // k-block counter across tiles
+      int s = 0;  // stage ring position / phase, continuous across tiles
+      uint32_t ph = 0;
       for (long long ti = 0; ti < my_tiles; ++ti) {
         long long m_pair;
         int n_tile;
         pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
         const int row0 = static_cast<int>(m_pair * 256 + static_cast<long long>(rank) * BM);
         const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);
-        for (int kb = 0; kb < kblocks; ++kb, ++g) {
-          const int s = static_cast<int>(g % Cfg::STAGES);
-          const uint32_t ph = static_cast<uint32_t>((g / Cfg::STAGES) & 1);
+        for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
           mbar_expect_tx(&full[s], Cfg::A_B + 2 * Cfg::B_B);
           tma_load_2d(&map_a, &full[s], st, kb * BK, row0);
           tma_load_2d(&map_bhi, &full[s], st + 2 * Cfg::A_B, kb * BK, brow0);
           tma_load_2d(&map_blo, &full[s], st + 2 * Cfg::A_B + Cfg::B_B, kb * BK, brow0);
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       constexpr uint32_t idesc = tf32_idesc_pair<kPairBN>();
-      long long g = 0;
+      int s = 0;
+      uint32_t ph = 0;
       for (long long q = 0; q < total_chunks; ++q) {
         const int c = static_cast<int>(q % nchunks);
         const int buf = static_cast<int>(q & 1);
@@ -563,9 +564,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
         const int kb_end = min(kblocks, (c + 1) * p.chunk);
-        for (int kb = c * p.chunk; kb < kb_end; ++kb, ++g) {
-          const int s = static_cast<int>(g % Cfg::STAGES);
-          const uint32_t ph = static_cast<uint32_t>((g / Cfg::STAGES) & 1);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
           mbar_wait_cluster(&conv[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
@@ -582,6 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             umma2_tf32(d, a_lo + adv, b_hi + adv, idesc, 1u);
           }
           umma2_commit_both(&empty[s]);
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
         umma2_commit_both(&acc_full[buf]);
       }
@@ -598,7 +598,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
     const int shift = sa + sb;
     float local = 0.f;
-    long long g = 0;
+    int s = 0;
+    uint32_t ph = 0;
     // Flat software pipeline over this pair's chunks: convert chunk q, then
     // promote chunk q-1 (complete by then), and after a tile's last chunk
     // write its epilogue -- the MMA meanwhile works on the next tile.
@@ -606,9 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (q < total_chunks) {
         const int c = static_cast<int>(q % nchunks);
         const int kb_end = min(kblocks, (c + 1) * p.chunk);
-        for (int kb = c * p.chunk; kb < kb_end; ++kb, ++g) {
-          const int s = static_cast<int>(g % Cfg::STAGES);
-          const uint32_t ph = static_cast<uint32_t>((g / Cfg::STAGES) & 1);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
           mbar_wait(&full[s], ph);
           float4* a = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES);
           float4* alo = reinterpret_cast<float4*>(smem + s * Cfg::STAGE_BYTES + Cfg::A_B);
@@ -632,8 +631,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             alo[idx] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) arrive_leader(&conv[s], rank);
+          // One cluster-scope arrival per CTA (it costs a GPU-scope membar).
+          asm volatile("bar.sync 1, %0;" ::"n"(kWorkers) : "memory");
+          if (wt == 0) arrive_leader(&conv[s], rank);
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
       }
       if (q >= 1) {
@@ -649,8 +650,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) arrive_leader(&acc_empty[buf], rank);
+        asm volatile("bar.sync 1, %0;" ::"n"(kWorkers) : "memory");
+        if (wt == 0) arrive_leader(&acc_empty[buf], rank);
         if (qq % nchunks == nchunks - 1) {  // tile complete: epilogue
           long long m_pair;
           int n_tile;

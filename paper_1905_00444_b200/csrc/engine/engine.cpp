@@ -78,12 +78,18 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
     check(cudaSetDevice(opt_.device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
   }
-  // Node layout = fold layout (open label at axis 0, bonds in gate order).
-  std::vector<int> x1(static_cast<std::size_t>(c.num_qubits()), 0);
-  for (int q : plan_.open_qubits) x1[static_cast<std::size_t>(q)] = -1;
-  shape_ = fold_worldlines(c, x1).shape();
-  if (shape_.open_qubits != plan_.open_qubits)
-    throw std::invalid_argument("engine: plan open qubits do not match the circuit fold");
+  // Device-side fold: the worldline fold with EVERY output wire left open is
+  // independent of x1; projecting a closed output onto bit b is taking half
+  // b of axis 0 (src/network.cpp:138-147), i.e. a view offset.  So the open
+  // fold is uploaded once per engine and an x1 batch only moves node views.
+  const int nq = c.num_qubits();
+  for (int q : plan_.open_qubits)
+    if (q < 0 || q >= nq) throw std::invalid_argument("engine: plan open qubits do not match the circuit fold");
+  GridNetwork open_fold = fold_worldlines(c, std::vector<int>(static_cast<std::size_t>(nq), -1));
+  shape_ = open_fold.shape();
+  closed_.assign(static_cast<std::size_t>(nq), 1);
+  for (int q : plan_.open_qubits) closed_[static_cast<std::size_t>(q)] = 0;
+  node_x1_off_.assign(static_cast<std::size_t>(nq), 0);
   batch_ = std::int64_t{1} << plan_.open_qubits.size();
   compile();
   pack_buffers();
@@ -95,9 +101,14 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
   check(cudaMemset(metas_, 0, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta memset");
   check(cudaMalloc(&acc_, sizeof(double2) * static_cast<std::size_t>(batch_)), "acc cudaMalloc");
   check(cudaMemset(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_)), "acc memset");
-  check(cudaHostAlloc(reinterpret_cast<void**>(&staging_), static_cast<std::size_t>(std::max<std::int64_t>(node_bytes_, 8)),
-                      cudaHostAllocDefault),
-        "pinned staging");
+  {  // one-time upload of the open fold (x1-independent node tensors)
+    std::vector<cfloat> host(static_cast<std::size_t>(node_bytes_ / 8), cfloat{});
+    for (std::size_t q = 0; q < open_fold.nodes.size(); ++q)
+      std::copy(open_fold.nodes[q].data.begin(), open_fold.nodes[q].data.end(),
+                host.begin() + static_cast<std::ptrdiff_t>(node_elem_off_[q]));
+    check(cudaMemcpy(arena_ + bufs_[0].offset, host.data(), static_cast<std::size_t>(node_bytes_), cudaMemcpyHostToDevice),
+          "node upload");
+  }
   op_ms_.assign(ops_.size(), 0.0);
   op_execs_.assign(ops_.size(), 0);
   set_profile(opt_.profile);
@@ -121,7 +132,6 @@ Engine::~Engine() {
   if (metas_) cudaFree(metas_);
   if (acc_) cudaFree(acc_);
   if (per_slice_) cudaFree(per_slice_);
-  if (staging_) cudaFreeHost(staging_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -132,6 +142,7 @@ void Engine::compile() {
   node_vol_.assign(n, 0);
   node_full_strides_.assign(n, {});
   node_cut_axes_.assign(n, {});
+  node_wire_stride_.assign(n, 0);
   std::int64_t elems = 0;
   for (std::size_t q = 0; q < n; ++q) {
     node_elem_off_[q] = elems;
@@ -153,7 +164,9 @@ void Engine::compile() {
     v.off = node_elem_off_[q];
     v.node = static_cast<int>(q);
     std::vector<int> cut_axes(fixed, -1);
-    for (std::size_t a = 0; a < node.labels.size(); ++a) {
+    // Axis 0 is the output wire; a closed output is a per-x1 half offset.
+    node_wire_stride_[q] = node_full_strides_[q][0];
+    for (std::size_t a = closed_[q] ? 1 : 0; a < node.labels.size(); ++a) {
       auto it = std::find(plan_.cut.labels.begin(), plan_.cut.labels.begin() + static_cast<std::ptrdiff_t>(fixed),
                           node.labels[a]);
       if (it != plan_.cut.labels.begin() + static_cast<std::ptrdiff_t>(fixed)) {
@@ -460,30 +473,14 @@ std::int64_t Engine::prepare(const std::vector<int>& x1_bits) {
   if (static_cast<int>(x1_bits.size()) != circuit_.num_qubits())
     throw std::invalid_argument("fold: bitstring length != qubit count");
   std::vector<int> open;
-  for (std::size_t q = 0; q < x1_bits.size(); ++q)
+  for (std::size_t q = 0; q < x1_bits.size(); ++q) {
     if (x1_bits[q] < 0) open.push_back(static_cast<int>(q));
-  if (open != plan_.open_qubits) throw std::invalid_argument("x1 open qubits do not match the plan's open qubits");
-  GridNetwork net = fold_worldlines(circuit_, x1_bits);
-  std::vector<std::vector<cfloat>> data;
-  data.reserve(net.nodes.size());
-  for (auto& t : net.nodes) data.push_back(std::move(t.data));
-  return prepare_nodes(data);
-}
-
-std::int64_t Engine::prepare_nodes(const std::vector<std::vector<cfloat>>& data) {
-  if (data.size() != node_vol_.size()) throw std::invalid_argument("prepare_nodes: node count mismatch");
-  check(cudaSetDevice(opt_.device), "cudaSetDevice");
-  // The staging buffer may still feed an in-flight copy.
-  check(cudaStreamSynchronize(stream_), "staging sync");
-  for (std::size_t q = 0; q < data.size(); ++q) {
-    if (static_cast<std::int64_t>(data[q].size()) != node_vol_[q])
-      throw std::invalid_argument("prepare_nodes: node volume mismatch");
-    std::memcpy(staging_ + node_elem_off_[q], data[q].data(), data[q].size() * sizeof(cfloat));
+    else if (x1_bits[q] > 1) throw std::invalid_argument("fold: output bits must be 0, 1 or -1 (open)");
   }
-  check(cudaMemcpyAsync(arena_ + bufs_[0].offset, staging_, static_cast<std::size_t>(node_bytes_),
-                        cudaMemcpyHostToDevice, stream_),
-        "node upload");
-  return node_bytes_;
+  if (open != plan_.open_qubits) throw std::invalid_argument("x1 open qubits do not match the plan's open qubits");
+  for (std::size_t q = 0; q < x1_bits.size(); ++q)
+    node_x1_off_[q] = closed_[q] ? x1_bits[q] * node_wire_stride_[q] : 0;
+  return 0;  // node tensors are resident; x1 only selects views
 }
 
 void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot) {
@@ -546,7 +543,7 @@ void Engine::run(const std::vector<std::int64_t>& slice_ids, bool reset, bool pe
   if (events_pending_) profile();  // fold finished timings before reusing events
   for (std::size_t s = 0; s < slice_ids.size(); ++s) {
     const auto digits = cut_digits(shape_, plan_.cut, slice_ids[s]);
-    std::vector<std::int64_t> node_off(node_vol_.size(), 0);
+    std::vector<std::int64_t> node_off(node_x1_off_);
     for (std::size_t q = 0; q < node_vol_.size(); ++q)
       for (std::size_t ci = 0; ci < node_cut_axes_[q].size(); ++ci) {
         const int ax = node_cut_axes_[q][ci];

@@ -3,9 +3,11 @@
 // src/sampler.cpp:17-36, and run_amplitudes, src/engine.cpp:300-378).
 //
 // A plan is compiled ONCE into a static device program:
-//   * node tensors live in one region of a single HBM arena (uploaded per
-//     x1 batch from pinned staging); a cut is a per-slice base offset plus
-//     dropped strides, so apply_cut costs nothing;
+//   * node tensors live in one region of a single HBM arena: the worldline
+//     fold with every output wire open, uploaded ONCE per circuit; an x1
+//     batch projects closed outputs by a half offset on axis 0 and a cut is
+//     a per-slice base offset plus dropped strides, so neither fold nor
+//     apply_cut moves data per batch or slice;
 //   * each plan step becomes [K1 permute of an operand when its layout is
 //     unusable] + one K2 CGEMM writing C = [lfree, rfree].  The executor
 //     picks the contracted-label order and N/T operand layouts that avoid
@@ -66,13 +68,11 @@ class Engine {
   cudaStream_t stream() const { return stream_; }
   int device() const { return opt_.device; }
 
-  // Folds the circuit for x1 (one entry per qubit, -1 exactly on the plan's
-  // open qubits) on the host and uploads the node tensors (async H2D from
-  // pinned staging).  Returns the H2D byte count.
+  // Selects the x1 batch (one entry per qubit, -1 exactly on the plan's open
+  // qubits).  The open fold is resident (uploaded once by the constructor),
+  // so this only sets per-node view offsets: no fold, no H2D.  Returns the
+  // H2D byte count (0).
   std::int64_t prepare(const std::vector<int>& x1_bits);
-  // Uploads pre-folded node tensors given in fold layout (tests / device
-  // fold).  data[q] has the node's full (uncut) volume.
-  std::int64_t prepare_nodes(const std::vector<std::vector<cfloat>>& data);
 
   // Runs the slices in the given order on the engine stream (async).
   // reset: zero the batch accumulator first.  per_slice: keep every
@@ -138,7 +138,9 @@ class Engine {
   std::vector<std::int64_t> node_elem_off_, node_vol_;
   std::vector<std::vector<std::int64_t>> node_full_strides_;
   std::vector<std::vector<int>> node_cut_axes_;  // per node: fixed cut index -> axis
-  std::vector<std::pair<int, std::int64_t>> cut_terms_;  // unused placeholder
+  std::vector<std::int64_t> node_wire_stride_;   // stride of axis 0 (the output wire)
+  std::vector<char> closed_;                     // 1 = output projected by x1
+  std::vector<std::int64_t> node_x1_off_;        // per-node view offset of the current x1
   std::int64_t node_bytes_ = 0;
 
   std::vector<Buffer> bufs_;
@@ -151,7 +153,6 @@ class Engine {
   double2* per_slice_ = nullptr;
   std::int64_t per_slice_cap_ = 0;
   std::int64_t per_slice_used_ = 0;
-  cfloat* staging_ = nullptr;
   std::int64_t launches_ = 0;
 
   std::vector<cudaEvent_t> ev_;
