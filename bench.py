@@ -48,6 +48,16 @@ CONFIGS = {
 }
 
 
+def tc_split(step):
+    """Operand split the tcgen05 path uses for a GEMM step (mirrors use_f16 in
+    csrc/device/cgemm_tc.cu): 3xFP16 on the CTA-pair kernel when 2k % 64 == 0."""
+    if os.environ.get("QSG_TC_PREC") == "tf32":
+        return "3xTF32"
+    n2 = 2 * step["n"]
+    pair = step["m"] % 256 == 0 and any(n2 % bn == 0 for bn in (256, 128, 64, 32))
+    return "3xFP16" if pair and (2 * step["k"]) % 32 == 0 else "3xTF32"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -290,17 +300,21 @@ def run_ours(args):
     clk = clocks.summary()
     smx = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * smx * 1e6 / 1e12
-    tc_peak = peaks["bf16_tflops"] / 2.0 / 3.0  # Eq.1-equivalent ceiling of 3xTF32 (tf32 = bf16/2, 3 passes)
-    if top["tensor_cores"]:
-        bound, peak_val, peak_note = "tensor", tc_peak, (f"3xTF32 ceiling = {peak_src} bf16 dense "
-                                                         f"{peaks['bf16_tflops']} TF/s / 2 (tf32) / 3 (passes)")
+    split = tc_split(top)
+    if top["tensor_cores"] and split == "3xFP16":
+        # Eq.1-equivalent ceiling of the 3-pass fp16 split (f16 rate = bf16 rate)
+        bound, peak_val, peak_note = "tensor", peaks["bf16_tflops"] / 3.0, (
+            f"3xFP16 ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 3 (passes)")
+    elif top["tensor_cores"]:
+        bound, peak_val, peak_note = "tensor", peaks["bf16_tflops"] / 2.0 / 3.0, (
+            f"3xTF32 ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 2 (tf32) / 3 (passes)")
     else:
         bound, peak_val, peak_note = "tensor", fp32_peak, (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x "
                                                            f"{smx:.0f} MHz ({peak_src} sm_max_mhz)")
     perm_ms = sum(p["ms_total"] for p in perms)
     perm_bytes = sum(p["bytes"] * p["executions"] for p in perms)
     roof = {"bound": bound, "achieved": achieved, "peak": peak_val, "unit": "TFLOP/s", "frac": achieved / peak_val,
-            "traffic": None, "kernel": ("cgemm_tc" if top["tensor_cores"] else "cgemm_simt") +
+            "traffic": None, "kernel": (f"cgemm_tc ({split})" if top["tensor_cores"] else "cgemm_simt") +
             f" step s{top['step']:03d} m={top['m']} n={top['n']} k={top['k']}",
             "kernel_share_of_step": top["ms_total"] / total_ms, "peak_source": peak_note,
             "fp32_simt_peak_tflops": fp32_peak,

@@ -37,6 +37,7 @@
 //              columns each), and the epilogue: apply the operands' pending
 //              power-of-two renormalisation, max|c|^2 -> TMeta, store C.
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -91,6 +92,7 @@ struct TcParams {
   TMeta* meta_c;
   int norm_a, norm_b;
   int chunk;   // k-blocks per TMEM promotion chunk
+  int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
   unsigned char col_pos[24];
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using Cfg = TcCfg<BN>;
   constexpr int HALF = BN / 2;  // accumulator columns owned by one worker thread
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KiB aligned, still __shared__
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* conv = full + Cfg::STAGES;
   uint64_t* empty = conv + Cfg::STAGES;
@@ -484,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using Cfg = Tc2Cfg<kPairBN>;
   constexpr int HALF = kPairBN / 2;  // accumulator columns per worker thread
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KiB aligned, still __shared__
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
   uint64_t* conv = full + Cfg::STAGES;
   uint64_t* empty = conv + Cfg::STAGES;
@@ -719,6 +721,397 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// 3xFP16 CTA-pair kernel (default for CTA-pair shapes with 2k % 64 == 0).
+// Same persistent pipeline as cgemm_tc2_kernel, but each operand is split
+// as x * 2^e = hi + lo with hi, lo fp16 and e a per-operand power of two
+// that puts max|x| just below 2^15 (from the operand's device max |z|^2).
+// hi and lo carry 11 + 11 significand bits (as 3xTF32 does) and the
+// products run at the f16 tensor-core rate, twice the tf32 rate; the
+// epilogue removes 2^-(ea+eb) exactly.  Elements more than 2^16 below the
+// operand's max lose relative precision in lo gradually (subnormal fp16),
+// i.e. their absolute error stays below 2^-39 max|x| -- far under FP32's
+// normwise error for these sums.
+// Stage layout (per CTA): raw A fp32 [128 rows x 64] as two SW128 TMA boxes
+// of 32 columns, each converted IN PLACE to interleaved hi / lo SW64 atoms
+// (32 fp16 = 64 B per row), then the pre-expanded B_r^T hi / lo fp16
+// planes (SW128, 64 fp16 per row).
+constexpr int BK16 = 64;  // real K per stage of the fp16 kernel
+constexpr std::int64_t kF16Scratch = 256;  // workspace head: two TMeta operand-maximum slots
+
+__device__ __forceinline__ int f16_exp(const TMeta* m) {
+  if (m == nullptr) return 0;
+  const unsigned bits = m->maxsq_bits;
+  if (bits == 0 || bits >= 0x7f800000u) return 0;
+  int e = 0;
+  frexpf(sqrtf(__uint_as_float(bits)), &e);  // max|z| = f * 2^e, f in [0.5, 1)
+  return 15 - e;
+}
+
+// K-major, SWIZZLE_64B descriptor (rows of 64 B, 8-row atoms of 512 B at a
+// 1 KiB stride: the hi and lo atoms of one 8-row group are interleaved).
+__device__ __forceinline__ uint64_t kmajor_sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(4) << 61;           // SWIZZLE_64B
+  return d;
+}
+
+template <int BN>
+__host__ __device__ constexpr uint32_t f16_idesc_pair() {
+  return (1u << 4)                 // D format F32
+         | (0u << 7) | (0u << 10)  // A, B format F16
+         | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// 8 fp32 (scaled by s) -> 8 fp16 hi + 8 fp16 lo, x*s = hi + lo (+ O(2^-22)).
+__device__ __forceinline__ void split_f16x8(const float4& a, const float4& b, float s, uint4& hi, uint4& lo) {
+  const float x[8] = {a.x * s, a.y * s, a.z * s, a.w * s, b.x * s, b.y * s, b.z * s, b.w * s};
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __half2 hh = __floats2half2_rn(x[2 * j], x[2 * j + 1]);
+    const float2 hf = __half22float2(hh);
+    h[j] = h2_bits(hh);
+    l[j] = h2_bits(__floats2half2_rn(x[2 * j] - hf.x, x[2 * j + 1] - hf.y));
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+template <int BN>
+struct Tc5Cfg {
+  static constexpr int A_B = BM * BK16 * 4;        // raw fp32 A tile = hi0|lo0|hi1|lo1 after conversion
+  static constexpr int B_B = (BN / 2) * BK16 * 2;  // one fp16 plane of this CTA's half of B_r^T
+  static constexpr int STAGE_BYTES = A_B + 2 * B_B;
+  static constexpr int EPI_PITCH = 20;
+  static constexpr int EPI_BYTES = (kWorkers / 32) * 32 * EPI_PITCH * 4;
+  static constexpr int STAGES =
+      ((224 * 1024 - EPI_BYTES) / STAGE_BYTES) > 6 ? 6 : ((224 * 1024 - EPI_BYTES) / STAGE_BYTES);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static_assert(STAGES >= 2, "shared memory budget");
+};
+
+template <int kPairBN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
+                          const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
+  using Cfg = Tc5Cfg<kPairBN>;
+  constexpr int HALF = kPairBN / 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KiB aligned, still __shared__
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* conv = full + Cfg::STAGES;
+  uint64_t* empty = conv + Cfg::STAGES;
+  uint64_t* acc_full = empty + Cfg::STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const long long cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const long long m_pairs = p.m / 256;
+  const long long total = m_pairs * p.n_tiles;
+  const long long my_tiles = cluster < total ? (total - 1 - cluster) / nclusters + 1 : 0;
+
+  if (threadIdx.x == 0) {
+    // conv / acc_empty: one arrival per worker warp; the leader's also
+    // count the peer's relayed arrival.
+    const uint32_t cnt = kWorkers / 32 + (rank == 0 ? 1 : 0);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], cnt);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], cnt);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_bhi) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_blo) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "n"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base_slot;
+  const int kblocks = p.kblocks;
+  const int nchunks = (kblocks + p.chunk - 1) / p.chunk;
+  const long long total_chunks = my_tiles * nchunks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long ti = 0; ti < my_tiles; ++ti) {
+        long long m_pair;
+        int n_tile;
+        pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
+        const int row0 = static_cast<int>(m_pair * 256 + static_cast<long long>(rank) * BM);
+        const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          const bool tail = p.half_tail && kb == kblocks - 1;
+          mbar_expect_tx(&full[s], tail ? Cfg::STAGE_BYTES - Cfg::A_B / 2 : Cfg::STAGE_BYTES);
+          tma_load_2d(&map_a, &full[s], st, kb * BK16, row0);
+          if (!tail) tma_load_2d(&map_a, &full[s], st + Cfg::A_B / 2, kb * BK16 + BK16 / 2, row0);
+          tma_load_2d(&map_bhi, &full[s], st + Cfg::A_B, kb * BK16, brow0);
+          tma_load_2d(&map_blo, &full[s], st + Cfg::A_B + Cfg::B_B, kb * BK16, brow0);
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = f16_idesc_pair<kPairBN>();
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long q = 0; q < total_chunks; ++q) {
+        const int c = static_cast<int>(q % nchunks);
+        const int buf = static_cast<int>(q & 1);
+        mbar_wait_cluster(&acc_empty[buf], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
+        const int kb_end = min(kblocks, (c + 1) * p.chunk);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
+          mbar_wait_cluster(&conv[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
+          const uint64_t b_hi = kmajor_sw128_desc(st + Cfg::A_B);
+          const uint64_t b_lo = kmajor_sw128_desc(st + Cfg::A_B + Cfg::B_B);
+          const bool first = kb == c * p.chunk;
+#pragma unroll
+          for (int kk = 0; kk < BK16 / 16; ++kk) {
+            if (kk == 2 && p.half_tail && kb == kblocks - 1) break;  // B's zero-filled half is not needed
+            const uint32_t abox = st + (kk >> 1) * (Cfg::A_B / 2) + (kk & 1) * 32;
+            const uint64_t a_hi = kmajor_sw64_desc(abox);
+            const uint64_t a_lo = kmajor_sw64_desc(abox + 512);
+            const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);
+            umma2_f16(d, a_hi, b_hi + adv, idesc, (first && kk == 0) ? 0u : 1u);
+            umma2_f16(d, a_hi, b_lo + adv, idesc, 1u);
+            umma2_f16(d, a_lo, b_hi + adv, idesc, 1u);
+          }
+          umma2_commit_both(&empty[s]);
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        }
+        umma2_commit_both(&acc_full[buf]);
+      }
+    } else if (lane == 0) {
+      // Peer CTA: relay its workers' (CTA-scope, cheap) arrivals to the
+      // leader's barriers.  The cluster-scope release this needs costs a
+      // GPU-scope membar; issued here, by a thread with no outstanding
+      // global stores, it stays off the worker warps' critical path.
+      int s = 0;
+      uint32_t ph = 0;
+      for (long long q = 0; q <= total_chunks; ++q) {
+        if (q < total_chunks) {
+          const int c = static_cast<int>(q % nchunks);
+          const int kb_end = min(kblocks, (c + 1) * p.chunk);
+          for (int kb = c * p.chunk; kb < kb_end; ++kb) {
+            mbar_wait(&conv[s], ph);
+            mbar_arrive_remote(&conv[s], 0);
+            if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+          }
+        }
+        if (q >= 1) {
+          const long long qq = q - 1;
+          const int buf = static_cast<int>(qq & 1);
+          mbar_wait(&acc_empty[buf], static_cast<uint32_t>((qq >> 1) & 1));
+          mbar_arrive_remote(&acc_empty[buf], 0);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    float acc[HALF];
+#pragma unroll
+    for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
+    const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
+    const int ea = f16_exp(p.meta_a), eb = f16_exp(p.meta_b);
+    const int shift = sa + sb;            // the reference's renormalisation (recorded in log_scale)
+    const int unscale = shift + ea + eb;  // + the fp16 operand scaling
+    const float scale_a = scalbnf(1.f, ea);
+    float local = 0.f;
+    int s = 0;
+    uint32_t ph = 0;
+    for (long long q = 0; q <= total_chunks; ++q) {
+      if (q < total_chunks) {
+        const int c = static_cast<int>(q % nchunks);
+        const int kb_end = min(kblocks, (c + 1) * p.chunk);
+        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
+          mbar_wait(&full[s], ph);
+          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          // In place, warp-local: each 8-row group g of a box (1 KiB of raw
+          // fp32) becomes its hi (512 B) and lo (512 B) SW64 atoms, so A_hi
+          // / A_lo are 8-row atoms at a 1 KiB stride (SBO) and no warp
+          // touches another warp's rows.  Lane = (row rl, 8-column group cg).
+          {
+            const int rl = lane >> 2, cg = lane & 3;
+            const int iters = (p.half_tail && kb == kblocks - 1 ? 1 : 2) * (BM / 8) / (kWorkers / 32);
+#pragma unroll 1
+            for (int it = 0; it < iters; ++it) {
+              const int gi = it * (kWorkers / 32) + (warp - 2);  // 0..31 over both boxes
+              uint8_t* grp = st + (gi >> 4) * (Cfg::A_B / 2) + (gi & 15) * 1024;
+              const float4 x0 = *reinterpret_cast<const float4*>(grp + rl * 128 + (((2 * cg) ^ rl) << 4));
+              const float4 x1 = *reinterpret_cast<const float4*>(grp + rl * 128 + (((2 * cg + 1) ^ rl) << 4));
+              __syncwarp();
+              uint4 h, l;
+              split_f16x8(x0, x1, scale_a, h, l);
+              const int off = rl * 64 + ((cg ^ ((rl >> 1) & 3)) << 4);
+              *reinterpret_cast<uint4*>(grp + off) = h;
+              *reinterpret_cast<uint4*>(grp + 512 + off) = l;
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);  // this warp's rows are converted
+          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+        }
+      }
+      if (q >= 1) {
+        const long long qq = q - 1;
+        const int buf = static_cast<int>(qq & 1);
+        mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < HALF / 16; ++j) {
+          float v[16];
+          tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + 16 * j), v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        if (qq % nchunks == nchunks - 1) {
+          long long m_pair;
+          int n_tile;
+          pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
+          const long long row_base = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32;
+          float* base = p.c + row_base * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF;
+          float* stg = epi_stage + (warp - 2) * 32 * Cfg::EPI_PITCH;
+          long long my_row_off = 0, col_tile_off = 0;
+          if (p.store_perm) {
+            const long long grow = row_base + lane;
+            for (int b = 0; b < p.nrow_bits; ++b)
+              if ((grow >> b) & 1) my_row_off += 1ll << p.row_pos[b];
+            const long long gcol = (static_cast<long long>(n_tile) * kPairBN + half * HALF) / 2;
+            for (int b = 0; b < p.ncol_bits; ++b)
+              if ((gcol >> b) & 1) col_tile_off += 1ll << p.col_pos[b];
+          }
+#pragma unroll
+          for (int c0 = 0; c0 < HALF; c0 += 16) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 v = make_float4(scalbnf(acc[c0 + 4 * i], -unscale), scalbnf(acc[c0 + 4 * i + 1], -unscale),
+                                           scalbnf(acc[c0 + 4 * i + 2], -unscale),
+                                           scalbnf(acc[c0 + 4 * i + 3], -unscale));
+              local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
+              *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
+            }
+            __syncwarp();
+            long long jc_off = 0;
+            if (p.store_perm) {
+              const int jloc = (c0 >> 1) + 2 * (lane & 3);
+              for (int b = 0; b < 7 && b < p.ncol_bits; ++b)
+                if ((jloc >> b) & 1) jc_off += 1ll << p.col_pos[b];
+            }
+#pragma unroll
+            for (int it = 0; it < 4; ++it) {
+              const int r = it * 8 + (lane >> 2), c4 = lane & 3;
+              const float4 v = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 4 * c4);
+              if (p.store_perm) {
+                const long long ro = __shfl_sync(0xffffffffu, my_row_off, r);
+                *reinterpret_cast<float4*>(p.c + 2 * (ro + col_tile_off + jc_off)) = v;
+              } else {
+                *reinterpret_cast<float4*>(base + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) = v;
+              }
+            }
+            __syncwarp();
+          }
+#pragma unroll
+          for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+        }
+      }
+    }
+    if (p.meta_c) {
+      for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+      if (lane == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
+      if (blockIdx.x == 0 && threadIdx.x == 64)
+        p.meta_c->log_scale = (p.meta_a ? p.meta_a->log_scale : 0.0) + (p.meta_b ? p.meta_b->log_scale : 0.0) + shift;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
+  }
+}
+
+// B (complex) -> B_r^T hi / lo fp16 planes [2n][2k] scaled by 2^eb.
+__global__ void __launch_bounds__(256) tc_prep_b_f16_kernel(const float2* __restrict__ b, __half* __restrict__ hi,
+                                                            __half* __restrict__ lo, long long n, long long k, int tb,
+                                                            const TMeta* __restrict__ meta_b) {
+  __shared__ float2 tile[32][33];
+  const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    if (!tb) {
+      const long long p = p0 + r, j = j0 + tx;
+      tile[r][tx] = (p < k && j < n) ? b[p * n + j] : make_float2(0.f, 0.f);
+    } else {
+      const long long j = j0 + r, p = p0 + tx;
+      tile[tx][r] = (p < k && j < n) ? b[j * k + p] : make_float2(0.f, 0.f);
+    }
+  }
+  __syncthreads();
+  const float s = scalbnf(1.f, f16_exp(meta_b));
+  const long long k2 = 2 * k;
+  for (int r = ty; r < 32; r += 8) {
+    const long long j = j0 + r, p = p0 + tx;
+    if (j >= n || p >= k) continue;
+    const float2 v = tile[tx][r];
+    const float re = v.x * s, im = v.y * s;
+    const __half2 h0 = __floats2half2_rn(re, -im), h1 = __floats2half2_rn(im, re);
+    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+    const long long row0 = (2 * j) * k2 + 2 * p, row1 = (2 * j + 1) * k2 + 2 * p;
+    *reinterpret_cast<__half2*>(hi + row0) = h0;
+    *reinterpret_cast<__half2*>(hi + row1) = h1;
+    *reinterpret_cast<__half2*>(lo + row0) = __floats2half2_rn(re - f0.x, -im - f0.y);
+    *reinterpret_cast<__half2*>(lo + row1) = __floats2half2_rn(im - f1.x, re - f1.y);
+  }
+}
+
 // B (complex, [k][n] or [n][k]) -> B_r^T hi/lo planes [2n][2k] fp32.
 __global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict__ b, float* __restrict__ hi,
                                                         float* __restrict__ lo, long long n, long long k, int tb,
@@ -797,6 +1190,20 @@ CUtensorMap make_map(const void* base, long long cols, long long rows, int box_r
   return m;
 }
 
+// fp16 map: inner dim `cols` (contiguous), box [box_rows x 64] (128 B), SW128.
+CUtensorMap make_map_f16(const void* base, long long cols, long long rows, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK16), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
+  return m;
+}
+
 int chunk_blocks() {
   const char* env = std::getenv("QSG_TC_CHUNK");
   const int v = env ? std::atoi(env) : kChunkDefault;
@@ -864,6 +1271,49 @@ cudaError_t launch_pair(const GemmArgs& g, const float* bhi, const float* blo, c
   return cudaGetLastError();
 }
 
+// Operand precision of the CTA-pair path: 3xFP16 with power-of-two operand
+// scaling (default) or 3xTF32 (QSG_TC_PREC=tf32).
+bool use_f16(std::int64_t m, std::int64_t n, std::int64_t k) {
+  const char* env = std::getenv("QSG_TC_PREC");
+  if (env && std::strcmp(env, "tf32") == 0) return false;
+  return use_pair(m, n) && (2 * k) % (BK16 / 2) == 0;
+}
+
+template <int BN>
+cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta* meta_b, const __half* bhi,
+                            const __half* blo, cudaStream_t stream) {
+  const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
+  const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, BN / 2);
+  const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, BN / 2);
+  TcParams p{};
+  p.c = static_cast<float*>(g.c);
+  p.m = g.m;
+  p.n2 = 2 * g.n;
+  p.kblocks = static_cast<int>((2 * g.k + BK16 - 1) / BK16);
+  p.half_tail = (2 * g.k) % BK16 != 0 ? 1 : 0;
+  p.meta_a = meta_a;
+  p.meta_b = meta_b;
+  p.meta_c = g.meta_c;
+  p.norm_a = g.norm_a && g.meta_a != nullptr;
+  p.norm_b = g.norm_b && g.meta_b != nullptr;
+  p.chunk = std::max(1, chunk_blocks() / 2);  // promotion interval in real K stays 128
+  p.store_perm = g.store_perm ? 1 : 0;
+  p.nrow_bits = g.nrow_bits;
+  p.ncol_bits = g.ncol_bits;
+  std::memcpy(p.row_pos, g.row_pos, sizeof p.row_pos);
+  std::memcpy(p.col_pos, g.col_pos, sizeof p.col_pos);
+  const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
+  p.n_tiles = static_cast<int>((2 * g.n) / BN);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg<BN>::SMEM);
+  });
+  const long long clusters = std::min<long long>(pairs, pair_slots());
+  cgemm_f16_pair_kernel<BN>
+      <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mbh, mbl, p);
+  return cudaGetLastError();
+}
+
 int tc_bn(std::int64_t n) {
   const char* env = std::getenv("QSG_TC_BN");
   const int want = env ? std::atoi(env) : 256;
@@ -905,8 +1355,9 @@ bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t 
   return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n);
 }
 
-std::int64_t cgemm_tc_workspace_bytes(std::int64_t /*m*/, std::int64_t n, std::int64_t k, bool, bool) {
-  return 2 * (2 * n) * (2 * k) * 4;  // B_r^T hi + lo
+std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool) {
+  if (use_f16(m, n, k)) return kF16Scratch + 2 * (2 * n) * (2 * k) * 2;  // operand maxima + fp16 B_r^T hi + lo
+  return 2 * (2 * n) * (2 * k) * 4;                                     // fp32 B_r^T hi + lo
 }
 
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
@@ -914,6 +1365,46 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     throw std::invalid_argument("cgemm_tc: shape not supported by the tensor-core path");
   if (g.workspace == nullptr || g.workspace_bytes < cgemm_tc_workspace_bytes(g.m, g.n, g.k, g.trans_a, g.trans_b))
     throw std::invalid_argument("cgemm_tc: workspace too small");
+  if (g.store_perm && !use_pair(g.m, g.n))
+    throw std::invalid_argument("cgemm_tc: fused output permutation needs the CTA-pair path");
+  if (g.store_perm && !use_pair(g.m, g.n))
+    throw std::invalid_argument("cgemm_tc: fused output permutation needs the CTA-pair path");
+  if (use_f16(g.m, g.n, g.k)) {
+    // Operand maxima for the fp16 scaling: the producers' device metas when
+    // present, else a max |z|^2 scan into workspace scratch.
+    TMeta* scratch = static_cast<TMeta*>(g.workspace);
+    const TMeta* ma = g.meta_a;
+    const TMeta* mb = g.meta_b;
+    if (!ma || !mb) {
+      cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * sizeof(TMeta), stream);
+      if (e != cudaSuccess) return e;
+    }
+    if (!ma) {
+      cudaError_t e = max_abs_sq(g.a, g.m * g.k, scratch, stream, launches);
+      if (e != cudaSuccess) return e;
+      ma = scratch;
+    }
+    if (!mb) {
+      cudaError_t e = max_abs_sq(g.b, g.n * g.k, scratch + 1, stream, launches);
+      if (e != cudaSuccess) return e;
+      mb = scratch + 1;
+    }
+    __half* bhi = reinterpret_cast<__half*>(static_cast<char*>(g.workspace) + kF16Scratch);
+    __half* blo = bhi + (2 * g.n) * (2 * g.k);
+    dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
+    tc_prep_b_f16_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k,
+                                                    g.trans_b ? 1 : 0, mb);
+    if (launches) ++*launches;
+    cudaError_t e = cudaSuccess;
+    switch (pair_bn(g.n)) {
+      case 256: e = launch_f16_pair<256>(g, ma, mb, bhi, blo, stream); break;
+      case 128: e = launch_f16_pair<128>(g, ma, mb, bhi, blo, stream); break;
+      case 64: e = launch_f16_pair<64>(g, ma, mb, bhi, blo, stream); break;
+      default: e = launch_f16_pair<32>(g, ma, mb, bhi, blo, stream); break;
+    }
+    if (launches) ++*launches;
+    return e;
+  }
   float* bhi = static_cast<float*>(g.workspace);
   float* blo = bhi + (2 * g.n) * (2 * g.k);
   {

@@ -138,11 +138,16 @@ def test_cgemm_device_shapes_vs_fp64(gpu, m, n, k, ta, tb):
 @pytest.mark.parametrize("m,n,k,tb", [(128, 64, 16, 0), (256, 128, 64, 0), (1024, 256, 256, 0), (512, 192, 80, 1),
                                       (4096, 128, 1024, 0), (1 << 15, 256, 256, 0),
                                       # narrow-N CTA-pair variants (BN = 32 / 64 / 128 real columns)
-                                      (1 << 14, 16, 256, 0), (2048, 32, 64, 1), (1024, 64, 512, 0), (768, 48, 32, 0)])
-def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb):
-    """tcgen05 3xTF32 path: FP32-level accuracy (1e-5 relative Frobenius, the
-    reference's TTGT tolerance, test_tensor.cpp:120-155)."""
+                                      (1 << 14, 16, 256, 0), (2048, 32, 64, 1), (1024, 64, 512, 0), (768, 48, 32, 0),
+                                      # fp16 kernel with a half k-block tail (2k % 64 == 32)
+                                      (512, 128, 16, 0), (1024, 64, 48, 1), (256, 32, 80, 0)])
+@pytest.mark.parametrize("prec", ["f16", "tf32"])
+def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb, prec, monkeypatch):
+    """tcgen05 path (3xFP16 with operand scaling on CTA-pair shapes, 3xTF32
+    otherwise or with QSG_TC_PREC=tf32): FP32-level accuracy (1e-5 relative
+    Frobenius, the reference's TTGT tolerance, test_tensor.cpp:120-155)."""
     import torch
+    monkeypatch.setenv("QSG_TC_PREC", prec)
     g = torch.Generator().manual_seed(m + 3 * n + 7 * k)
     A = torch.complex(torch.rand(m, k, generator=g) - 0.5, torch.rand(m, k, generator=g) - 0.5)
     B = torch.complex(torch.rand(k, n, generator=g) - 0.5, torch.rand(k, n, generator=g) - 0.5)
@@ -160,3 +165,29 @@ def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb):
     gpu._check(gpu.lib().qsg_cgemm_dev(dA.data_ptr(), dB.data_ptr(), dC2.data_ptr(), m, n, k, 0, tb, None))
     torch.cuda.synchronize()
     assert float((dC2.cpu().to(torch.complex128) - got).abs().norm() / want.abs().norm()) < 1e-5
+
+
+@pytest.mark.parametrize("prec", ["f16", "tf32"])
+def test_cgemm_tensor_core_dynamic_range(gpu, prec, monkeypatch):
+    """Rows of A spanning 2^0 .. 2^-30 and a B with tiny entries: the fp16
+    split's per-operand power-of-two scaling keeps every row whose scale is
+    within 2^-14 of the operand max at FP32-level relative accuracy, and
+    the rest within an absolute error far below FP32's normwise error."""
+    import torch
+    monkeypatch.setenv("QSG_TC_PREC", prec)
+    m, n, k = 1024, 128, 256
+    g = torch.Generator().manual_seed(11)
+    A = torch.complex(torch.rand(m, k, generator=g) - 0.5, torch.rand(m, k, generator=g) - 0.5)
+    B = torch.complex(torch.rand(k, n, generator=g) - 0.5, torch.rand(k, n, generator=g) - 0.5) * 2.0 ** -40
+    rs = torch.tensor([2.0 ** -(i % 31) for i in range(m)])
+    A = A * rs[:, None]
+    want = A.to(torch.complex128) @ B.to(torch.complex128)
+    dC = torch.zeros(m, n, dtype=torch.complex64, device="cuda")
+    gpu._check(gpu.lib().qsg_cgemm_tc_dev(A.cuda().data_ptr(), B.cuda().data_ptr(), dC.data_ptr(), m, n, k, 0, None))
+    torch.cuda.synchronize()
+    got = dC.cpu().to(torch.complex128)
+    row_err = (got - want).abs().norm(dim=1) / want.abs().norm(dim=1)
+    near = torch.tensor([(i % 31) <= 14 for i in range(m)])
+    assert float(row_err[near].max()) < 1e-5
+    abs_err = float((got - want).abs().max() / want.abs().max())
+    assert abs_err < 5e-6
