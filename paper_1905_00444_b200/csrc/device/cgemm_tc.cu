@@ -40,6 +40,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -92,6 +93,7 @@ struct TcParams {
   TMeta* meta_c;
   int norm_a, norm_b;
   int chunk;   // k-blocks per TMEM promotion chunk
+  int group_m;    // m-pairs per rasterization group (fp16 kernel)
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
@@ -466,10 +468,10 @@ __host__ __device__ constexpr uint32_t tf32_idesc_pair() {
 // expanded-B columns they stream are shared through L2 (n-fastest order
 // re-read all of B_r^T from HBM per wave of m tiles: 1.2 TB per s026 launch).
 __device__ __forceinline__ void pair_tile_coords(long long t, long long m_pairs, int n_tiles, long long& m_pair,
-                                                 int& n_tile) {
-  const long long span = static_cast<long long>(kGroupM) * n_tiles;
-  const long long first_m = (t / span) * kGroupM;
-  const long long gsize = min(static_cast<long long>(kGroupM), m_pairs - first_m);
+                                                 int& n_tile, int group_m = kGroupM) {
+  const long long span = static_cast<long long>(group_m) * n_tiles;
+  const long long first_m = (t / span) * group_m;
+  const long long gsize = min(static_cast<long long>(group_m), m_pairs - first_m);
   const long long within = t % span;
   m_pair = first_m + within % gsize;
   n_tile = static_cast<int>(within / gsize);
@@ -871,7 +873,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (long long ti = 0; ti < my_tiles; ++ti) {
         long long m_pair;
         int n_tile;
-        pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
+        pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
         const int row0 = static_cast<int>(m_pair * 256 + static_cast<long long>(rank) * BM);
         const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);
         for (int kb = 0; kb < kblocks; ++kb) {
@@ -1015,7 +1017,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (qq % nchunks == nchunks - 1) {
           long long m_pair;
           int n_tile;
-          pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile);
+          pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
           const long long row_base = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32;
           float* base = p.c + row_base * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF;
           float* stg = epi_stage + (warp - 2) * 32 * Cfg::EPI_PITCH;
@@ -1204,6 +1206,12 @@ CUtensorMap make_map_f16(const void* base, long long cols, long long rows, int b
   return m;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* env = std::getenv(name);
+  const int v = env ? std::atoi(env) : dflt;
+  return v >= 1 ? v : dflt;
+}
+
 int chunk_blocks() {
   const char* env = std::getenv("QSG_TC_CHUNK");
   const int v = env ? std::atoi(env) : kChunkDefault;
@@ -1223,6 +1231,24 @@ long long pair_slots() {
     return static_cast<long long>(std::max(1, sms / 2));
   }();
   return n;
+}
+
+// Co-resident CTA pairs of a pair kernel (GPCs with an odd number of free
+// SMs cannot host a pair on their last SM): the persistent grid must not
+// exceed it, or the surplus clusters run as a serial tail wave.
+template <typename Kern>
+long long resident_pairs(Kern kernel, int smem) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pair_slots()));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, reinterpret_cast<const void*>(kernel), &cfg) != cudaSuccess || n <= 0) {
+    cudaGetLastError();
+    n = static_cast<int>(pair_slots());
+  }
+  if (std::getenv("QSG_TC_DEBUG")) std::fprintf(stderr, "qsg: %d co-resident CTA pairs (smem %d)\n", n, smem);
+  return std::min<long long>(n, pair_slots());
 }
 
 // The CTA-pair kernel covers 256 x 256 (real) tiles; QSG_TC_2SM=0 disables it.
@@ -1262,11 +1288,11 @@ cudaError_t launch_pair(const GemmArgs& g, const float* bhi, const float* blo, c
   std::memcpy(p.col_pos, g.col_pos, sizeof p.col_pos);
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static const long long slots = [] {
     cudaFuncSetAttribute(cgemm_tc2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg<BN>::SMEM);
-  });
-  const long long clusters = std::min<long long>(pairs, pair_slots());
+    return resident_pairs(cgemm_tc2_kernel<BN>, Tc2Cfg<BN>::SMEM);
+  }();
+  const long long clusters = std::min<long long>(pairs, slots);
   cgemm_tc2_kernel<BN><<<static_cast<unsigned>(2 * clusters), kThreads, Tc2Cfg<BN>::SMEM, stream>>>(ma, mbh, mbl, p);
   return cudaGetLastError();
 }
@@ -1291,6 +1317,7 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.n2 = 2 * g.n;
   p.kblocks = static_cast<int>((2 * g.k + BK16 - 1) / BK16);
   p.half_tail = (2 * g.k) % BK16 != 0 ? 1 : 0;
+  p.group_m = env_int("QSG_TC_GROUPM", kGroupM);
   p.meta_a = meta_a;
   p.meta_b = meta_b;
   p.meta_c = g.meta_c;
@@ -1304,11 +1331,11 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   std::memcpy(p.col_pos, g.col_pos, sizeof p.col_pos);
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static const long long slots = [] {
     cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg<BN>::SMEM);
-  });
-  const long long clusters = std::min<long long>(pairs, pair_slots());
+    return resident_pairs(cgemm_f16_pair_kernel<BN>, Tc5Cfg<BN>::SMEM);
+  }();
+  const long long clusters = std::min<long long>(pairs, slots);
   cgemm_f16_pair_kernel<BN>
       <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mbh, mbl, p);
   return cudaGetLastError();
