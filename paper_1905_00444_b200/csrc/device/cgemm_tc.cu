@@ -94,6 +94,9 @@ struct TcParams {
   int norm_a, norm_b;
   int chunk;   // k-blocks per TMEM promotion chunk
   int group_m;    // m-pairs per rasterization group (fp16 kernel)
+  unsigned int* sync;  // fp16 kernel: per-(wave, checkpoint) arrival counters (null: no K-sync)
+  int sync_every;      // k-blocks between checkpoints
+  int nclusters_hint;  // unused padding
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
@@ -876,7 +879,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
         const int row0 = static_cast<int>(m_pair * 256 + static_cast<long long>(rank) * BM);
         const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);
+        // K-sync: the producers of one wave of tiles stay within two
+        // checkpoints of each other, so the A / B k-slabs they share are
+        // still in L2 when the last of them reads it (unsynchronised
+        // pairs drift apart by more than L2 holds and re-stream from HBM).
+        const int ncheck = kblocks / max(p.sync_every, 1) + 1;
+        const unsigned need = 2u * static_cast<unsigned>(min(nclusters, total - ti * nclusters));
+        unsigned int* ctr = p.sync ? p.sync + ti * ncheck : nullptr;
         for (int kb = 0; kb < kblocks; ++kb) {
+          if (ctr && kb % p.sync_every == 0) {
+            const int c = kb / p.sync_every;
+            atomicAdd(ctr + c, 1u);
+            if (c >= 1) {
+              for (int spin = 0; spin < 4096; ++spin) {  // bounded: never a deadlock, at worst unsynchronised
+                unsigned v;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr + c - 1) : "memory");
+                if (v >= need) break;
+                __nanosleep(128);
+              }
+            }
+          }
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
           const bool tail = p.half_tail && kb == kblocks - 1;
@@ -1083,7 +1105,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // B (complex) -> B_r^T hi / lo fp16 planes [2n][2k] scaled by 2^eb.
 __global__ void __launch_bounds__(256) tc_prep_b_f16_kernel(const float2* __restrict__ b, __half* __restrict__ hi,
                                                             __half* __restrict__ lo, long long n, long long k, int tb,
-                                                            const TMeta* __restrict__ meta_b) {
+                                                            const TMeta* __restrict__ meta_b, long long pitch) {
   __shared__ float2 tile[32][33];
   const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1098,7 +1120,6 @@ __global__ void __launch_bounds__(256) tc_prep_b_f16_kernel(const float2* __rest
   }
   __syncthreads();
   const float s = scalbnf(1.f, f16_exp(meta_b));
-  const long long k2 = 2 * k;
   for (int r = ty; r < 32; r += 8) {
     const long long j = j0 + r, p = p0 + tx;
     if (j >= n || p >= k) continue;
@@ -1106,7 +1127,7 @@ __global__ void __launch_bounds__(256) tc_prep_b_f16_kernel(const float2* __rest
     const float re = v.x * s, im = v.y * s;
     const __half2 h0 = __floats2half2_rn(re, -im), h1 = __floats2half2_rn(im, re);
     const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
-    const long long row0 = (2 * j) * k2 + 2 * p, row1 = (2 * j + 1) * k2 + 2 * p;
+    const long long row0 = (2 * j) * pitch + 2 * p, row1 = (2 * j + 1) * pitch + 2 * p;
     *reinterpret_cast<__half2*>(hi + row0) = h0;
     *reinterpret_cast<__half2*>(hi + row1) = h1;
     *reinterpret_cast<__half2*>(lo + row0) = __floats2half2_rn(re - f0.x, -im - f0.y);
@@ -1177,6 +1198,17 @@ EncodeFn encode_fn() {
   return fn;
 }
 
+CUtensorMapL2promotion l2_promo() {
+  const char* env = std::getenv("QSG_TC_L2PROMO");
+  if (!env) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  switch (std::atoi(env)) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 // 2-D fp32 K-major map: inner dim `cols` (contiguous), outer `rows`; box
 // [box_rows x 32] with 128-byte swizzle.
 CUtensorMap make_map(const void* base, long long cols, long long rows, int box_rows) {
@@ -1186,22 +1218,28 @@ CUtensorMap make_map(const void* base, long long cols, long long rows, int box_r
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
 }
 
+// Row pitch (elements) of the fp16 B_r^T planes: 2k plus QSG_TC_BPAD (experiment).
+long long b16_pitch(std::int64_t k) {
+  const char* env = std::getenv("QSG_TC_BPAD");
+  return 2 * k + (env ? std::atoll(env) : 0);
+}
+
 // fp16 map: inner dim `cols` (contiguous), box [box_rows x 64] (128 B), SW128.
-CUtensorMap make_map_f16(const void* base, long long cols, long long rows, int box_rows) {
+CUtensorMap make_map_f16(const void* base, long long cols, long long rows, long long pitch, int box_rows) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 2};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK16), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
 }
@@ -1305,12 +1343,28 @@ bool use_f16(std::int64_t m, std::int64_t n, std::int64_t k) {
   return use_pair(m, n) && (2 * k) % (BK16 / 2) == 0;
 }
 
+// K-sync checkpoint spacing in k-blocks (QSG_TC_SYNC; 0 disables).
+int sync_every() {
+  const char* env = std::getenv("QSG_TC_SYNC");
+  return env ? std::max(0, std::atoi(env)) : 16;
+}
+
+// Counters for every (wave, checkpoint); waves <= tiles.  0 when K-sync is
+// off or the K loop is too short to drift.
+std::int64_t sync_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
+  const int every = sync_every();
+  const std::int64_t kblocks = (2 * k + BK16 - 1) / BK16;
+  if (every <= 0 || kblocks < 4 * every || !use_pair(m, n)) return 0;
+  const std::int64_t tiles = (m / 256) * ((2 * n) / pair_bn(n));
+  return ((tiles * (kblocks / every + 1) * 4 + 255) / 256) * 256;
+}
+
 template <int BN>
 cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta* meta_b, const __half* bhi,
-                            const __half* blo, cudaStream_t stream) {
+                            const __half* blo, unsigned int* sync, cudaStream_t stream) {
   const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
-  const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, BN / 2);
-  const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, BN / 2);
+  const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2);
+  const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2);
   TcParams p{};
   p.c = static_cast<float*>(g.c);
   p.m = g.m;
@@ -1318,6 +1372,8 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.kblocks = static_cast<int>((2 * g.k + BK16 - 1) / BK16);
   p.half_tail = (2 * g.k) % BK16 != 0 ? 1 : 0;
   p.group_m = env_int("QSG_TC_GROUPM", kGroupM);
+  p.sync = sync;
+  p.sync_every = sync_every();
   p.meta_a = meta_a;
   p.meta_b = meta_b;
   p.meta_c = g.meta_c;
@@ -1383,7 +1439,8 @@ bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t 
 }
 
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool) {
-  if (use_f16(m, n, k)) return kF16Scratch + 2 * (2 * n) * (2 * k) * 2;  // operand maxima + fp16 B_r^T hi + lo
+  if (use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo
+    return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2;
   return 2 * (2 * n) * (2 * k) * 4;                                     // fp32 B_r^T hi + lo
 }
 
@@ -1416,18 +1473,24 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
       if (e != cudaSuccess) return e;
       mb = scratch + 1;
     }
-    __half* bhi = reinterpret_cast<__half*>(static_cast<char*>(g.workspace) + kF16Scratch);
-    __half* blo = bhi + (2 * g.n) * (2 * g.k);
+    const std::int64_t sb = sync_bytes(g.m, g.n, g.k);
+    unsigned int* sync = sb > 0 ? reinterpret_cast<unsigned int*>(static_cast<char*>(g.workspace) + kF16Scratch) : nullptr;
+    if (sync) {
+      cudaError_t e = cudaMemsetAsync(sync, 0, static_cast<size_t>(sb), stream);
+      if (e != cudaSuccess) return e;
+    }
+    __half* bhi = reinterpret_cast<__half*>(static_cast<char*>(g.workspace) + kF16Scratch + sb);
+    __half* blo = bhi + (2 * g.n) * b16_pitch(g.k);
     dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
     tc_prep_b_f16_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k,
-                                                    g.trans_b ? 1 : 0, mb);
+                                                    g.trans_b ? 1 : 0, mb, b16_pitch(g.k));
     if (launches) ++*launches;
     cudaError_t e = cudaSuccess;
     switch (pair_bn(g.n)) {
-      case 256: e = launch_f16_pair<256>(g, ma, mb, bhi, blo, stream); break;
-      case 128: e = launch_f16_pair<128>(g, ma, mb, bhi, blo, stream); break;
-      case 64: e = launch_f16_pair<64>(g, ma, mb, bhi, blo, stream); break;
-      default: e = launch_f16_pair<32>(g, ma, mb, bhi, blo, stream); break;
+      case 256: e = launch_f16_pair<256>(g, ma, mb, bhi, blo, sync, stream); break;
+      case 128: e = launch_f16_pair<128>(g, ma, mb, bhi, blo, sync, stream); break;
+      case 64: e = launch_f16_pair<64>(g, ma, mb, bhi, blo, sync, stream); break;
+      default: e = launch_f16_pair<32>(g, ma, mb, bhi, blo, sync, stream); break;
     }
     if (launches) ++*launches;
     return e;
