@@ -290,6 +290,11 @@ def run_ours(args):
     eng.run(slices_for(0), reset=True)
     prof = eng.profile()
     eng.set_profile(False)
+    if args.profile_out and rank == 0:
+        with open(args.profile_out, "w") as f:
+            for p in sorted(prof, key=lambda p: -p["ms_total"]):
+                if p["executions"] > 0:
+                    f.write(json.dumps(p) + "\n")
     peaks, peak_src = load_peaks()
     gemms = [p for p in prof if p["kind"] == 1 and p["executions"] > 0]
     perms = [p for p in prof if p["kind"] == 0 and p["executions"] > 0]
@@ -377,6 +382,7 @@ def main():
                     help="BASELINE config: 1, 2 (default, the metric's workload), 3/4 (Bristlecone stand-ins), 5")
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-out", default="", help="write the per-op profile (one JSON line per op) here")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--cpu-budget-flops", type=float, default=4e11,
                     help="Eq.1 flops per task of the reference CPU sample (plan prefix)")

@@ -138,6 +138,16 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+// CTA-pair TMA: data lands in this CTA's smem, complete_tx goes to the
+// barrier at shared::cluster address `bar` (the leader's).
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+
 // K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms
 // of 1024 B; SBO = 1024 B; version 1; layout type 2 = SWIZZLE_128B).
 __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
@@ -772,13 +782,35 @@ __host__ __device__ constexpr uint32_t f16_idesc_pair() {
          | (static_cast<uint32_t>(BN >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred;
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n\t}"
+      : "=r"(pred));
+  return pred;
+}
+
+// Issued only by the lane with do_it != 0 (operands warp-uniform).
+__device__ __forceinline__ void umma2_f16_if(uint32_t do_it, uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 e, %5, 0;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(do_it));
+}
+
+__device__ __forceinline__ void umma2_commit_both_if(uint32_t do_it, uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "setp.ne.b32 e, %2, 0;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(0x3)), "r"(do_it)
+      : "memory");
 }
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
@@ -812,10 +844,16 @@ struct Tc5Cfg {
   static_assert(STAGES >= 2, "shared memory budget");
 };
 
-template <int kPairBN>
+// kSplitA: A arrives pre-split (fp16 hi / lo planes, tc_prep_a_f16_kernel or
+// a producer epilogue), so the stage is TMA -> MMA with no worker pass:
+// both CTAs' TMA loads complete on the leader's full[s] (cta_group::2) and
+// the worker warps only promote and store.  map_a is then the A_hi plane
+// and map_alo the A_lo plane (SW128, 64 fp16 per row).
+template <int kPairBN, bool kSplitA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
-                          const __grid_constant__ CUtensorMap map_blo, const TcParams p) {
+    cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_alo,
+                          const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
+                          const TcParams p) {
   using Cfg = Tc5Cfg<kPairBN>;
   constexpr int HALF = kPairBN / 2;
   extern __shared__ uint8_t smem_raw[];
@@ -853,6 +891,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    if (kSplitA) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_alo) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_bhi) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_blo) : "memory");
   }
@@ -901,6 +940,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
+          if constexpr (kSplitA) {
+            // Both CTAs' bytes complete on the leader's full[s].
+            uint32_t bar = smem_u32(&full[s]);
+            if (rank == 0) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
+            else asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(bar) : "r"(bar));
+            tma_load_2d_pair(&map_a, bar, st, kb * BK16, row0);
+            tma_load_2d_pair(&map_alo, bar, st + Cfg::A_B / 2, kb * BK16, row0);
+            tma_load_2d_pair(&map_bhi, bar, st + Cfg::A_B, kb * BK16, brow0);
+            tma_load_2d_pair(&map_blo, bar, st + Cfg::A_B + Cfg::B_B, kb * BK16, brow0);
+            if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+            continue;
+          }
           const bool tail = p.half_tail && kb == kblocks - 1;
           mbar_expect_tx(&full[s], tail ? Cfg::STAGE_BYTES - Cfg::A_B / 2 : Cfg::STAGE_BYTES);
           tma_load_2d(&map_a, &full[s], st, kb * BK16, row0);
@@ -912,39 +963,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {
+      // The whole warp runs the issue loop (warp-uniform descriptors stay
+      // in uniform registers); one elected lane issues each tcgen05 op.
       constexpr uint32_t idesc = f16_idesc_pair<kPairBN>();
-      int s = 0;
+      const uint32_t leader = elect_one();
+      int s = 0, c = 0;
       uint32_t ph = 0;
       for (long long q = 0; q < total_chunks; ++q) {
-        const int c = static_cast<int>(q % nchunks);
         const int buf = static_cast<int>(q & 1);
         mbar_wait_cluster(&acc_empty[buf], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
         const int kb_end = min(kblocks, (c + 1) * p.chunk);
         for (int kb = c * p.chunk; kb < kb_end; ++kb) {
-          mbar_wait_cluster(&conv[s], ph);
+          if constexpr (kSplitA) mbar_wait(&full[s], ph);
+          else mbar_wait_cluster(&conv[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
           const uint64_t b_hi = kmajor_sw128_desc(st + Cfg::A_B);
           const uint64_t b_lo = kmajor_sw128_desc(st + Cfg::A_B + Cfg::B_B);
+          const uint64_t a0 = kmajor_sw64_desc(st);
           const bool first = kb == c * p.chunk;
+          const int nkk = (p.half_tail && kb == kblocks - 1) ? 2 : BK16 / 16;  // zero-filled B half not needed
 #pragma unroll
           for (int kk = 0; kk < BK16 / 16; ++kk) {
-            if (kk == 2 && p.half_tail && kb == kblocks - 1) break;  // B's zero-filled half is not needed
-            const uint32_t abox = st + (kk >> 1) * (Cfg::A_B / 2) + (kk & 1) * 32;
-            const uint64_t a_hi = kmajor_sw64_desc(abox);
-            const uint64_t a_lo = kmajor_sw64_desc(abox + 512);
+            if (kk == nkk) break;
+            uint64_t a_hi, a_lo;
+            if constexpr (kSplitA) {  // SW128 planes: +32 B per K=16 step
+              a_hi = kmajor_sw128_desc(st) + static_cast<uint64_t>(kk * 2);
+              a_lo = kmajor_sw128_desc(st + Cfg::A_B / 2) + static_cast<uint64_t>(kk * 2);
+            } else {
+              a_hi = a0 + static_cast<uint64_t>(((kk >> 1) * (Cfg::A_B / 2) + (kk & 1) * 32) >> 4);
+              a_lo = a_hi + (512 >> 4);
+            }
             const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);
-            umma2_f16(d, a_hi, b_hi + adv, idesc, (first && kk == 0) ? 0u : 1u);
-            umma2_f16(d, a_hi, b_lo + adv, idesc, 1u);
-            umma2_f16(d, a_lo, b_hi + adv, idesc, 1u);
+            umma2_f16_if(leader, d, a_hi, b_hi + adv, idesc, (first && kk == 0) ? 0u : 1u);
+            umma2_f16_if(leader, d, a_hi, b_lo + adv, idesc, 1u);
+            umma2_f16_if(leader, d, a_lo, b_hi + adv, idesc, 1u);
           }
-          umma2_commit_both(&empty[s]);
+          umma2_commit_both_if(leader, &empty[s]);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
-        umma2_commit_both(&acc_full[buf]);
+        umma2_commit_both_if(leader, &acc_full[buf]);
+        if (++c == nchunks) c = 0;
       }
     } else if (lane == 0) {
       // Peer CTA: relay its workers' (CTA-scope, cheap) arrivals to the
@@ -954,7 +1016,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (long long q = 0; q <= total_chunks; ++q) {
-        if (q < total_chunks) {
+        if (!kSplitA && q < total_chunks) {
           const int c = static_cast<int>(q % nchunks);
           const int kb_end = min(kblocks, (c + 1) * p.chunk);
           for (int kb = c * p.chunk; kb < kb_end; ++kb) {
@@ -988,7 +1050,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     for (long long q = 0; q <= total_chunks; ++q) {
-      if (q < total_chunks) {
+      if (!kSplitA && q < total_chunks) {
         const int c = static_cast<int>(q % nchunks);
         const int kb_end = min(kblocks, (c + 1) * p.chunk);
         for (int kb = c * p.chunk; kb < kb_end; ++kb) {
@@ -1099,6 +1161,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
+  }
+}
+
+// A (complex, [m][k] = fp32 [m][2k]) -> A hi / lo fp16 planes [m][2k], scaled by 2^ea.
+__global__ void __launch_bounds__(256) tc_prep_a_f16_kernel(const float4* __restrict__ a, uint2* __restrict__ hi,
+                                                            uint2* __restrict__ lo, long long n4,
+                                                            const TMeta* __restrict__ meta_a) {
+  const float s = scalbnf(1.f, f16_exp(meta_a));
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n4; i += static_cast<long long>(gridDim.x) * 256) {
+    const float4 x = a[i];
+    const __half2 h0 = __floats2half2_rn(x.x * s, x.y * s), h1 = __floats2half2_rn(x.z * s, x.w * s);
+    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+    hi[i] = make_uint2(h2_bits(h0), h2_bits(h1));
+    lo[i] = make_uint2(h2_bits(__floats2half2_rn(x.x * s - f0.x, x.y * s - f0.y)),
+                       h2_bits(__floats2half2_rn(x.z * s - f1.x, x.w * s - f1.y)));
   }
 }
 
@@ -1359,10 +1436,20 @@ std::int64_t sync_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   return ((tiles * (kblocks / every + 1) * 4 + 255) / 256) * 256;
 }
 
+// Pre-split A (QSG_TC_SPLITA=1, experiment): a separate HBM pass converts A
+// to fp16 hi / lo planes so the GEMM's stages are pure TMA -> MMA.
+bool split_a(std::int64_t m, std::int64_t n, std::int64_t k) {
+  const char* env = std::getenv("QSG_TC_SPLITA");
+  return env && env[0] == '1' && use_f16(m, n, k) && (2 * k) % BK16 == 0;
+}
+
 template <int BN>
 cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta* meta_b, const __half* bhi,
-                            const __half* blo, unsigned int* sync, cudaStream_t stream) {
-  const CUtensorMap ma = make_map(g.a, 2 * g.k, g.m, BM);
+                            const __half* blo, unsigned int* sync, const __half* ahi, const __half* alo,
+                            cudaStream_t stream) {
+  const bool split = ahi != nullptr;
+  const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM) : make_map(g.a, 2 * g.k, g.m, BM);
+  const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM) : ma;
   const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2);
   const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2);
   TcParams p{};
@@ -1388,12 +1475,19 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
   static const long long slots = [] {
-    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg<BN>::SMEM);
-    return resident_pairs(cgemm_f16_pair_kernel<BN>, Tc5Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN>::SMEM);
+    return resident_pairs(cgemm_f16_pair_kernel<BN, false>, Tc5Cfg<BN>::SMEM);
   }();
   const long long clusters = std::min<long long>(pairs, slots);
-  cgemm_f16_pair_kernel<BN>
-      <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mbh, mbl, p);
+  if (split)
+    cgemm_f16_pair_kernel<BN, true>
+        <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  else
+    cgemm_f16_pair_kernel<BN, false>
+        <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   return cudaGetLastError();
 }
 
@@ -1439,8 +1533,8 @@ bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t 
 }
 
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool) {
-  if (use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo
-    return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2;
+  if (use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo (+ pre-split A hi + lo)
+    return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2 + (split_a(m, n, k) ? 8 * m * k : 0);
   return 2 * (2 * n) * (2 * k) * 4;                                     // fp32 B_r^T hi + lo
 }
 
@@ -1485,12 +1579,23 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     tc_prep_b_f16_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k,
                                                     g.trans_b ? 1 : 0, mb, b16_pitch(g.k));
     if (launches) ++*launches;
+    __half* ahi = nullptr;
+    __half* alo = nullptr;
+    if (split_a(g.m, g.n, g.k)) {
+      ahi = blo + (2 * g.n) * b16_pitch(g.k);
+      alo = ahi + g.m * 2 * g.k;
+      const long long n4 = g.m * 2 * g.k / 4;
+      const int blocks = static_cast<int>(std::min<long long>((n4 + 255) / 256, 148 * 16));
+      tc_prep_a_f16_kernel<<<blocks, 256, 0, stream>>>(static_cast<const float4*>(g.a), reinterpret_cast<uint2*>(ahi),
+                                                       reinterpret_cast<uint2*>(alo), n4, ma);
+      if (launches) ++*launches;
+    }
     cudaError_t e = cudaSuccess;
     switch (pair_bn(g.n)) {
-      case 256: e = launch_f16_pair<256>(g, ma, mb, bhi, blo, sync, stream); break;
-      case 128: e = launch_f16_pair<128>(g, ma, mb, bhi, blo, sync, stream); break;
-      case 64: e = launch_f16_pair<64>(g, ma, mb, bhi, blo, sync, stream); break;
-      default: e = launch_f16_pair<32>(g, ma, mb, bhi, blo, sync, stream); break;
+      case 256: e = launch_f16_pair<256>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
+      case 128: e = launch_f16_pair<128>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
+      case 64: e = launch_f16_pair<64>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
+      default: e = launch_f16_pair<32>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
     }
     if (launches) ++*launches;
     return e;
