@@ -1436,11 +1436,18 @@ std::int64_t sync_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   return ((tiles * (kblocks / every + 1) * 4 + 255) / 256) * 256;
 }
 
-// Pre-split A (QSG_TC_SPLITA=1, experiment): a separate HBM pass converts A
-// to fp16 hi / lo planes so the GEMM's stages are pure TMA -> MMA.
+// Pre-split A: a streaming pass converts A to fp16 hi / lo planes so the
+// GEMM's stages are pure TMA -> MMA (tensor pipe ~98% busy instead of ~68%
+// with the in-kernel conversion on the critical path).  The pass moves
+// 16 B per complex element of A; the GEMM spends ~8n flop on each, so it
+// pays from n ~ 1024 complex columns up (measured: s026 / s038 of config 2
+// and the 2^15 cubes of config 5 gain 20-30%, the n = 256 steps lose).
+// QSG_TC_SPLITA=0/1 forces it off/on (where the shape allows).
 bool split_a(std::int64_t m, std::int64_t n, std::int64_t k) {
+  if (!use_f16(m, n, k) || (2 * k) % BK16 != 0) return false;
   const char* env = std::getenv("QSG_TC_SPLITA");
-  return env && env[0] == '1' && use_f16(m, n, k) && (2 * k) % BK16 == 0;
+  if (env) return env[0] == '1';
+  return n >= 1024;
 }
 
 template <int BN>
@@ -1536,6 +1543,18 @@ std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64
   if (use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo (+ pre-split A hi + lo)
     return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2 + (split_a(m, n, k) ? 8 * m * k : 0);
   return 2 * (2 * n) * (2 * k) * 4;                                     // fp32 B_r^T hi + lo
+}
+
+double cgemm_tc_rate(std::int64_t m, std::int64_t n, std::int64_t k) {
+  if (split_a(m, n, k)) return 4.5e14;  // measured 450-630 TF/s (config 2 s026 / config 5 cubes)
+  if (use_f16(m, n, k)) return 3.5e14;  // in-kernel A conversion: ~68% tensor-pipe occupancy
+  return 1.5e14;                        // 3xTF32
+}
+
+double cgemm_tc_prep_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
+  const double nb = static_cast<double>(n) * static_cast<double>(k);  // complex elements of B
+  if (!use_f16(m, n, k)) return 40.0 * nb;                            // read 8, write 32 (fp32 hi + lo)
+  return 24.0 * nb + (split_a(m, n, k) ? 16.0 * static_cast<double>(m) * static_cast<double>(k) : 0.0);
 }
 
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {

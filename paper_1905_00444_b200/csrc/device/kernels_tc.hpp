@@ -18,6 +18,11 @@ bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool tran
 bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
+// Planning model of the tensor-core path for a shape: sustained Eq.(1)
+// flop/s and the HBM bytes of its operand preparation passes (B expansion,
+// A pre-split), for the engine's layout / role cost model.
+double cgemm_tc_rate(std::int64_t m, std::int64_t n, std::int64_t k);
+double cgemm_tc_prep_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
 // Process-wide switch (QSG_TENSOR_CORES=0 disables); the engine also has
 // a per-instance option.
 bool tc_enabled();

@@ -255,8 +255,8 @@ void Engine::compile() {
       double cost = 0.0;
     };
     const double flops = static_cast<double>(step.flops);
-    constexpr double kHbm = 5.0e12, kTcRate = 1.5e14, kSimtRate = 4.0e13;
-    constexpr std::int64_t kMaxTcWorkspace = std::int64_t{48} << 30;  // B_r^T hi+lo = 32 B per B element
+    constexpr double kHbm = 5.0e12, kSimtRate = 4.0e13;
+    constexpr std::int64_t kMaxTcWorkspace = std::int64_t{48} << 30;  // B_r^T planes (+ pre-split A planes)
     auto evaluate = [&](bool swap, const std::vector<Label>& con, bool force_permute_a) {
       const View& X = swap ? R : L;
       const View& Y = swap ? L : R;
@@ -277,8 +277,8 @@ void Engine::compile() {
       ch.tc = opt_.tensor_cores && dev::cgemm_tc_eligible(mm, nn2, k, ta, tb) &&
               dev::cgemm_tc_workspace_bytes(mm, nn2, k, ta, tb) <= kMaxTcWorkspace;
       const double bytes = (ch.use_a ? 0.0 : 16.0 * X.volume()) + (ch.use_b ? 0.0 : 16.0 * Y.volume()) +
-                           (ch.tc ? 40.0 * Y.volume() : 0.0);
-      ch.cost = bytes / kHbm + flops / (ch.tc ? kTcRate : kSimtRate);
+                           (ch.tc ? dev::cgemm_tc_prep_bytes(mm, nn2, k) : 0.0);
+      ch.cost = bytes / kHbm + flops / (ch.tc ? dev::cgemm_tc_rate(mm, nn2, k) : kSimtRate);
       return ch;
     };
     Choice best = evaluate(false, con_l, false);
