@@ -1046,6 +1046,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int shift = sa + sb;            // the reference's renormalisation (recorded in log_scale)
     const int unscale = shift + ea + eb;  // + the fp16 operand scaling
     const float scale_a = scalbnf(1.f, ea);
+    // 2^-unscale as one or two exact power-of-two factors (cheaper than
+    // scalbnf per element, same rounding: a single multiply by 2^u is exact
+    // unless the result is subnormal, which both round identically).
+    const int u1 = min(max(-unscale, -126), 127), u2 = -unscale - u1;
+    const float f1 = __int_as_float((127 + u1) << 23);
+    const float f2 = u2 == 0 ? 1.f : scalbnf(1.f, u2);
+    // Fused output permutation: the column part of a float4's offset is
+    // f(c0 / 2) + f(2 * (lane & 3)) (disjoint bits of the complex column).
+    long long lane_col_off = 0;
+    if (p.store_perm)
+      for (int b = 0; b < 3 && b < p.ncol_bits; ++b)
+        if (((2 * (lane & 3)) >> b) & 1) lane_col_off += 1ll << p.col_pos[b];
     float local = 0.f;
     int s = 0;
     uint32_t ph = 0;
@@ -1118,18 +1130,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int c0 = 0; c0 < HALF; c0 += 16) {
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              const float4 v = make_float4(scalbnf(acc[c0 + 4 * i], -unscale), scalbnf(acc[c0 + 4 * i + 1], -unscale),
-                                           scalbnf(acc[c0 + 4 * i + 2], -unscale),
-                                           scalbnf(acc[c0 + 4 * i + 3], -unscale));
+              float4 v = make_float4(acc[c0 + 4 * i] * f1, acc[c0 + 4 * i + 1] * f1, acc[c0 + 4 * i + 2] * f1,
+                                     acc[c0 + 4 * i + 3] * f1);
+              if (u2 != 0) { v.x *= f2; v.y *= f2; v.z *= f2; v.w *= f2; }
               local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
               *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
             }
             __syncwarp();
-            long long jc_off = 0;
+            long long jc_off = lane_col_off;
             if (p.store_perm) {
-              const int jloc = (c0 >> 1) + 2 * (lane & 3);
-              for (int b = 0; b < 7 && b < p.ncol_bits; ++b)
-                if ((jloc >> b) & 1) jc_off += 1ll << p.col_pos[b];
+              const int jhi = c0 >> 1;  // multiple of 8: column bits 3..6
+#pragma unroll
+              for (int b = 3; b < 7; ++b)
+                if (b < p.ncol_bits && ((jhi >> b) & 1)) jc_off += 1ll << p.col_pos[b];
             }
 #pragma unroll
             for (int it = 0; it < 4; ++it) {

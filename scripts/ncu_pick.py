@@ -16,8 +16,12 @@ def main():
     path, name = sys.argv[1], sys.argv[2]
     rs = [r for r in rows(path) if r["Metric Name"] == "gpu__time_duration.sum"]
     hits = [(i, float(r["Metric Value"])) for i, r in enumerate(x for x in rs if name in x["Kernel Name"])]
-    top = max(v for _, v in hits)
-    print(min(i for i, v in hits if v >= 0.95 * top))  # first launch of the longest step
+    rng = [float(a.split("=")[1]) * 1e6 for a in sys.argv if a.startswith("--ms=")]  # --ms=LO --ms=HI (ms)
+    if len(rng) == 2:
+        print(min(i for i, v in hits if rng[0] <= v <= rng[1]))  # first launch in the duration window
+    else:
+        top = max(v for _, v in hits)
+        print(min(i for i, v in hits if v >= 0.95 * top))  # first launch of the longest step
     if "--summary" in sys.argv:
         tot = defaultdict(float)
         for r in rs:
