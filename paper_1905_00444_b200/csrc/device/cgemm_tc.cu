@@ -96,7 +96,10 @@ struct TcParams {
   int group_m;    // m-pairs per rasterization group (fp16 kernel)
   unsigned int* sync;  // fp16 kernel: per-(wave, checkpoint) arrival counters (null: no K-sync)
   int sync_every;      // k-blocks between checkpoints
-  int nclusters_hint;  // unused padding
+  int a_presplit;      // fp16 kernel: A stored split (TMeta::split_exp), see GemmArgs
+  int c_split;         // fp16 kernel: write C split
+  int log2k;           // ceil(log2(k)): the split output's bound exponent
+  long long c_total;   // complex elements of C (offset of the lo plane / 4 bytes)
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
@@ -763,6 +766,14 @@ __device__ __forceinline__ int f16_exp(const TMeta* m) {
   return 15 - e;
 }
 
+// Exponent e with max|z| < 2^e from the meta's max |z|^2 (-1000: all zero).
+__device__ __forceinline__ int max_exp(const TMeta* m) {
+  if (m == nullptr || m->maxsq_bits == 0 || m->maxsq_bits >= 0x7f800000u) return -1000;
+  int e = 0;
+  frexpf(sqrtf(__uint_as_float(m->maxsq_bits)), &e);
+  return e;
+}
+
 // K-major, SWIZZLE_64B descriptor (rows of 64 B, 8-row atoms of 512 B at a
 // 1 KiB stride: the hi and lo atoms of one 8-row group are interleaved).
 __device__ __forceinline__ uint64_t kmajor_sw64_desc(uint32_t saddr) {
@@ -1042,7 +1053,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
     const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
-    const int ea = f16_exp(p.meta_a), eb = f16_exp(p.meta_b);
+    const int ea = p.a_presplit ? p.meta_a->split_exp : f16_exp(p.meta_a), eb = f16_exp(p.meta_b);
     const int shift = sa + sb;            // the reference's renormalisation (recorded in log_scale)
     const int unscale = shift + ea + eb;  // + the fp16 operand scaling
     const float scale_a = scalbnf(1.f, ea);
@@ -1052,6 +1063,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int u1 = min(max(-unscale, -126), 127), u2 = -unscale - u1;
     const float f1 = __int_as_float((127 + u1) << 23);
     const float f2 = u2 == 0 ? 1.f : scalbnf(1.f, u2);
+    // Split output: y = acc * 2^-t with |acc| <= 2k * max|A_s| * max|B_s| <
+    // 2^(log2k + 1 + EA + EB) (A_s, B_s: the scaled operands the MMA saw,
+    // EA / EB their exact max exponents), so t = log2k + 1 + EA + EB - 15
+    // keeps |y| below 2^15 without knowing C's max.  Using the operands'
+    // true maxima (not the 2^15 cap) keeps the headroom from compounding
+    // along chains of split hand-offs.  data = y * 2^-split_exp with
+    // split_exp = unscale - t.
+    int t_split = 0;
+    {
+      const int xa = max_exp(p.meta_a), xb = max_exp(p.meta_b);
+      if (xa > -1000 && xb > -1000) t_split = min(max(p.log2k + 1 + (xa + ea) + (xb + eb) - 15, -126), 126);
+    }
+    const float fy = __int_as_float((127 - t_split) << 23);
+    uint8_t* const c_bytes = reinterpret_cast<uint8_t*>(p.c);
+    const long long lo_plane = 4 * p.c_total;
     // Fused output permutation: the column part of a float4's offset is
     // f(c0 / 2) + f(2 * (lane & 3)) (disjoint bits of the complex column).
     long long lane_col_off = 0;
@@ -1134,6 +1160,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                      acc[c0 + 4 * i + 3] * f1);
               if (u2 != 0) { v.x *= f2; v.y *= f2; v.z *= f2; v.w *= f2; }
               local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
+              if (p.c_split)
+                v = make_float4(acc[c0 + 4 * i] * fy, acc[c0 + 4 * i + 1] * fy, acc[c0 + 4 * i + 2] * fy,
+                                acc[c0 + 4 * i + 3] * fy);
               *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
             }
             __syncwarp();
@@ -1148,11 +1177,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int it = 0; it < 4; ++it) {
               const int r = it * 8 + (lane >> 2), c4 = lane & 3;
               const float4 v = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 4 * c4);
+              long long o;  // complex offset of v.xy in C
               if (p.store_perm) {
                 const long long ro = __shfl_sync(0xffffffffu, my_row_off, r);
-                *reinterpret_cast<float4*>(p.c + 2 * (ro + col_tile_off + jc_off)) = v;
+                o = ro + col_tile_off + jc_off;
               } else {
-                *reinterpret_cast<float4*>(base + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) = v;
+                o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) >> 1;
+              }
+              if (p.c_split) {
+                const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
+                const float2 g0 = __half22float2(h0), g1 = __half22float2(h1);
+                *reinterpret_cast<uint2*>(c_bytes + 4 * o) = make_uint2(h2_bits(h0), h2_bits(h1));
+                *reinterpret_cast<uint2*>(c_bytes + lo_plane + 4 * o) =
+                    make_uint2(h2_bits(__floats2half2_rn(v.x - g0.x, v.y - g0.y)),
+                               h2_bits(__floats2half2_rn(v.z - g1.x, v.w - g1.y)));
+              } else {
+                *reinterpret_cast<float4*>(p.c + 2 * o) = v;
               }
             }
             __syncwarp();
@@ -1165,8 +1205,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (p.meta_c) {
       for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
       if (lane == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
-      if (blockIdx.x == 0 && threadIdx.x == 64)
+      if (blockIdx.x == 0 && threadIdx.x == 64) {
         p.meta_c->log_scale = (p.meta_a ? p.meta_a->log_scale : 0.0) + (p.meta_b ? p.meta_b->log_scale : 0.0) + shift;
+        if (p.c_split) p.meta_c->split_exp = unscale - t_split;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1481,6 +1523,12 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.group_m = env_int("QSG_TC_GROUPM", kGroupM);
   p.sync = sync;
   p.sync_every = sync_every();
+  p.a_presplit = g.a_presplit ? 1 : 0;
+  p.c_split = g.c_split ? 1 : 0;
+  int l2k = 0;
+  while ((std::int64_t{1} << l2k) < g.k) ++l2k;
+  p.log2k = l2k;
+  p.c_total = g.m * g.n;
   p.meta_a = meta_a;
   p.meta_b = meta_b;
   p.meta_c = g.meta_c;
@@ -1552,9 +1600,14 @@ bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t 
   return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n);
 }
 
-std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool) {
-  if (use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo (+ pre-split A hi + lo)
-    return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2 + (split_a(m, n, k) ? 8 * m * k : 0);
+bool cgemm_tc_split_ok(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
+  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n) && (2 * k) % BK16 == 0;
+}
+
+std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool, bool a_presplit) {
+  if (a_presplit || use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo (+ pre-split A)
+    return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2 +
+           (!a_presplit && split_a(m, n, k) ? 8 * m * k : 0);
   return 2 * (2 * n) * (2 * k) * 4;                                     // fp32 B_r^T hi + lo
 }
 
@@ -1573,13 +1626,16 @@ double cgemm_tc_prep_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
   if (!cgemm_tc_supported(g.m, g.n, g.k, g.trans_a, g.trans_b))
     throw std::invalid_argument("cgemm_tc: shape not supported by the tensor-core path");
-  if (g.workspace == nullptr || g.workspace_bytes < cgemm_tc_workspace_bytes(g.m, g.n, g.k, g.trans_a, g.trans_b))
+  if (g.workspace == nullptr || g.workspace_bytes < cgemm_tc_workspace_bytes(g.m, g.n, g.k, g.trans_a, g.trans_b, g.a_presplit))
     throw std::invalid_argument("cgemm_tc: workspace too small");
   if (g.store_perm && !use_pair(g.m, g.n))
     throw std::invalid_argument("cgemm_tc: fused output permutation needs the CTA-pair path");
   if (g.store_perm && !use_pair(g.m, g.n))
     throw std::invalid_argument("cgemm_tc: fused output permutation needs the CTA-pair path");
-  if (use_f16(g.m, g.n, g.k)) {
+  if ((g.a_presplit || g.c_split) && !cgemm_tc_split_ok(g.m, g.n, g.k, g.trans_a, g.trans_b))
+    throw std::invalid_argument("cgemm_tc: split operand storage needs the fp16 CTA-pair path");
+  if (g.a_presplit && g.meta_a == nullptr) throw std::invalid_argument("cgemm_tc: pre-split A needs its meta");
+  if (g.a_presplit || g.c_split || use_f16(g.m, g.n, g.k)) {
     // Operand maxima for the fp16 scaling: the producers' device metas when
     // present, else a max |z|^2 scan into workspace scratch.
     TMeta* scratch = static_cast<TMeta*>(g.workspace);
@@ -1613,7 +1669,10 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
     if (launches) ++*launches;
     __half* ahi = nullptr;
     __half* alo = nullptr;
-    if (split_a(g.m, g.n, g.k)) {
+    if (g.a_presplit) {
+      ahi = static_cast<__half*>(const_cast<void*>(g.a));
+      alo = ahi + 2 * g.m * g.k;
+    } else if (split_a(g.m, g.n, g.k)) {
       ahi = blo + (2 * g.n) * b16_pitch(g.k);
       alo = ahi + g.m * 2 * g.k;
       const long long n4 = g.m * 2 * g.k / 4;

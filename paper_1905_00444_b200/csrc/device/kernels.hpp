@@ -20,7 +20,9 @@ namespace qsg::dev {
 struct TMeta {
   double log_scale;
   unsigned int maxsq_bits;
-  unsigned int pad;
+  // When the tensor is stored pre-split (fp16 hi plane | lo plane, see
+  // GemmArgs::c_split): data = (hi + lo) * 2^-split_exp.
+  int split_exp;
 };
 
 // ---- K1: permute -----------------------------------------------------------
@@ -60,6 +62,15 @@ struct GemmArgs {
   int nrow_bits = 0, ncol_bits = 0;
   unsigned char row_pos[48] = {};
   unsigned char col_pos[24] = {};
+  // Pre-split operand storage (tcgen05 fp16 CTA-pair path only).  A tensor
+  // of N complex elements stored split occupies the same 8N bytes: an fp16
+  // hi plane (re, im interleaved) in the first 4N bytes and the lo plane in
+  // the last 4N, element o at byte 4o of each, value (hi + lo) *
+  // 2^-meta.split_exp.  c_split: the epilogue writes C this way (exponent
+  // from the operand bounds, so no second pass); a_presplit: A is read
+  // this way (no conversion pass or in-kernel conversion).
+  bool c_split = false;
+  bool a_presplit = false;
 };
 std::int64_t cgemm_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
 cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);

@@ -16,7 +16,11 @@ bool cgemm_tc_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool tra
 bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 // The fused output permutation is available (CTA-pair kernel path).
 bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
-std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
+std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b,
+                                      bool a_presplit = false);
+// The fp16 CTA-pair kernel handles the shape, so C may be written split /
+// A read pre-split (GemmArgs::c_split / a_presplit).
+bool cgemm_tc_split_ok(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
 // Planning model of the tensor-core path for a shape: sustained Eq.(1)
 // flop/s and the HBM bytes of its operand preparation passes (B expansion,

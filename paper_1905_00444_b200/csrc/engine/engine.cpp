@@ -3,6 +3,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -92,6 +93,7 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
   node_x1_off_.assign(static_cast<std::size_t>(nq), 0);
   batch_ = std::int64_t{1} << plan_.open_qubits.size();
   compile();
+  split_handoffs();
   pack_buffers();
   op_ms_.assign(ops_.size(), 0.0);
   op_execs_.assign(ops_.size(), 0);
@@ -433,6 +435,41 @@ void Engine::compile() {
   }
 }
 
+// GEMM -> GEMM hand-offs in split storage: when a tensor-core GEMM's output
+// is read by exactly one op, and that op is a tensor-core GEMM using it in
+// place as its A operand (N layout, whole tensor), the producer's epilogue
+// writes fp16 hi | lo planes and the consumer streams them with no
+// conversion (dev::GemmArgs::c_split / a_presplit).  QSG_TC_CSPLIT=0 turns
+// this off.
+void Engine::split_handoffs() {
+  const char* env = std::getenv("QSG_TC_CSPLIT");
+  if (!opt_.tensor_cores || (env && env[0] == '0')) return;
+  const char* only = std::getenv("QSG_TC_CSPLIT_ONLY");  // debugging: restrict to one producer step
+  for (std::size_t i = 0; i < ops_.size(); ++i) {
+    Op& pr = ops_[i];
+    if (pr.kind != 1 || !pr.tc || !dev::cgemm_tc_split_ok(pr.m, pr.n, pr.k, pr.ta, pr.tb)) continue;
+    if (only && (std::string(",") + only + ",").find("," + std::to_string(pr.step) + ",") == std::string::npos) continue;
+    int reader = -1, readers = 0;
+    for (std::size_t j = i + 1; j < ops_.size(); ++j) {
+      const Op& q = ops_[j];
+      const bool reads = (q.kind != 1 && q.src.buf == pr.c) || (q.kind == 1 && (q.a.buf == pr.c || q.b.buf == pr.c));
+      if (reads) {
+        ++readers;
+        reader = static_cast<int>(j);
+      }
+    }
+    if (readers != 1) continue;
+    Op& co = ops_[static_cast<std::size_t>(reader)];
+    if (co.kind != 1 || !co.tc || co.a.buf != pr.c || co.b.buf == pr.c || co.a.off != 0 || co.a.node >= 0 || co.ta ||
+        co.m * co.k != pr.m * pr.n || co.meta_a != pr.meta_c || !dev::cgemm_tc_split_ok(co.m, co.n, co.k, co.ta, co.tb))
+      continue;
+    pr.c_split = true;
+    co.a_presplit = true;
+    co.ws_bytes = dev::cgemm_tc_workspace_bytes(co.m, co.n, co.k, co.ta, co.tb, true);
+    if (co.ws >= 0) bufs_[static_cast<std::size_t>(co.ws)].bytes = align_up(std::max<std::int64_t>(co.ws_bytes, 8));
+  }
+}
+
 void Engine::pack_buffers() {
   // First-fit over lifetimes, largest buffers first within equal starts.
   std::vector<int> order(bufs_.size());
@@ -511,6 +548,8 @@ void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off,
     g.workspace = op.ws >= 0 ? arena_ + bufs_[static_cast<std::size_t>(op.ws)].offset : nullptr;
     g.workspace_bytes = op.ws_bytes;
     g.store_perm = op.store_perm;
+    g.c_split = op.c_split;
+    g.a_presplit = op.a_presplit;
     g.nrow_bits = op.nrow_bits;
     g.ncol_bits = op.ncol_bits;
     std::copy(op.row_pos.begin(), op.row_pos.end(), g.row_pos);
@@ -625,7 +664,8 @@ std::string Engine::describe() const {
     else if (op.kind == 1)
       os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << " flops " << op.flops
          << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes
-         << (op.store_perm ? " fused-store" : "") << "\n";
+         << (op.store_perm ? " fused-store" : "") << (op.c_split ? " split-out" : "")
+         << (op.a_presplit ? " split-in" : "") << "\n";
     else os << "  accumulate " << op.count << "\n";
   }
   return os.str();

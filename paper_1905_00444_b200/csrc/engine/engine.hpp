@@ -120,9 +120,12 @@ class Engine {
     int nrow_bits = 0, ncol_bits = 0;
     std::array<unsigned char, 48> row_pos{};
     std::array<unsigned char, 24> col_pos{};
+    bool c_split = false;     // C written as fp16 hi | lo planes (dev::GemmArgs::c_split)
+    bool a_presplit = false;  // A read as fp16 hi | lo planes
   };
 
   void compile();
+  void split_handoffs();
   void pack_buffers();
   void* ptr(const Operand& o, const std::vector<std::int64_t>& node_off) const;
   void launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot);

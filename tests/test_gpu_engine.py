@@ -145,7 +145,7 @@ def test_engine_rejects_bad_inputs(gpu, cases):
 
 def test_config2_full_size_tensor_core_vs_simt(gpu):
     """BASELINE config 2 at full size (7x7, 1+32+1, 1024-amplitude batch, 2
-    slices, 2.15e14 flop): the tcgen05 3xTF32 engine and the FP32-FFMA
+    slices, 2.15e14 flop): the tcgen05 (3xFP16 split) engine and the FP32-FFMA
     engine are independent GEMM implementations; they must agree within the
     north-star tolerance (1e-4 on |amp|, batch fidelity >= 1 - 1e-6).  Also
     checks the size-independent properties: Porter-Thomas scale of the batch
@@ -169,6 +169,26 @@ def test_config2_full_size_tensor_core_vs_simt(gpu):
     assert fid >= 1 - 1e-6
     # Porter-Thomas: E[2^n |a|^2] = 1 over random bitstrings (loose, 1024 samples)
     assert 0.8 < np.mean(np.abs(a) ** 2) * 2.0**49 < 1.25
+
+
+def test_split_handoffs_match_fp32_storage(gpu, monkeypatch):
+    """GEMM -> GEMM hand-offs in fp16 hi|lo split storage (config 2 has 13
+    chained ones, up to five in a row): same amplitudes as fp32 storage to
+    FP32-level accuracy, i.e. the bound-based output scaling does not lose
+    precision along chains."""
+    text = gpu.generate_rqc(7, 7, 32, 0)
+    plan = open(os.path.join(ROOT, "configs", "config2_plan.json")).read()
+    x1 = gpu.draw_x1(49, json.loads(plan)["open_qubits"], 0, 1)
+    res = {}
+    for split in ("1", "0"):
+        monkeypatch.setenv("QSG_TC_CSPLIT", split)
+        with gpu.Engine(text, plan, tensor_cores=True) as e:
+            desc = e.describe()
+            e.prepare(x1)
+            e.run([0], reset=True)
+            res[split] = e.results()
+        assert (desc.count("split-in") >= 10) == (split == "1")
+    assert rel(res["1"], res["0"]) < 5e-6
 
 
 def test_tensor_core_paths_forced_small_vs_oracle(gpu, monkeypatch):
