@@ -1601,7 +1601,8 @@ bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t 
 }
 
 bool cgemm_tc_split_ok(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
-  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n) && (2 * k) % BK16 == 0;
+  // Any fp16 pair shape (a half k-block tail reads zero-filled plane columns it never multiplies).
+  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n);
 }
 
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool, bool a_presplit) {
