@@ -8,6 +8,7 @@
 //   flop model Eq.(1)          include/qsim/contraction.hpp:43-56
 //   fraction / select_slices   proj/src/engine.cpp:26-37, 285-298
 #include <algorithm>
+#include <limits>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -27,6 +28,12 @@ std::uint64_t flop_count(std::uint64_t v0, std::uint64_t v1, std::uint64_t v2) {
   if (static_cast<unsigned __int128>(root) * root != prod)
     throw std::invalid_argument("flop_count: volume product is not a perfect square");
   return 8 * root;
+}
+
+double log2_volume(const TensorShape& t) {
+  double v = 0.0;
+  for (auto d : t.dims) v += std::log2(static_cast<double>(d));
+  return v;
 }
 
 std::int64_t step_working_set(std::int64_t l, std::int64_t r, std::int64_t o) {
@@ -193,6 +200,14 @@ void annotate_plan(const NetworkShape& shape, ContractionPlan& plan) {
     const TensorShape& a = li->second;
     const TensorShape& b = ri->second;
     TensorShape out = sorted_shape(merge_free(a, b));
+    // Overflow guard: the reference silently wraps int64
+    // volumes / uint64 flops here for large greedy plans.  Reject instead.
+    const double lo = log2_volume(out), la = log2_volume(a), lb = log2_volume(b);
+    if (lo >= 59.0)
+      throw std::length_error("plan: step " + step.out + " has rank " + std::to_string(out.labels.size()) +
+                              ": volume 2^" + std::to_string(static_cast<int>(lo)) + " overflows int64 bytes");
+    if (3.0 + 0.5 * (la + lb + lo) >= 63.0)
+      throw std::length_error("plan: step " + step.out + " flops overflow uint64");
 
     step.out_labels = out.labels;
     step.out_volume = out.volume();
@@ -232,25 +247,45 @@ std::vector<PlanStep> greedy_steps(const NetworkShape& shape) {
   for (std::size_t q = 0; q < shape.nodes.size(); ++q) pool.emplace_back(node_name(static_cast<int>(q)), shape.nodes[q]);
   std::vector<PlanStep> steps;
   int next = 0;
+  // Candidate cost: exact (volume, flops) while they fit (the reference's
+  // keys, so small plans are identical); past 2^60 elements the reference
+  // wraps int64 / uint128 -- here such candidates sort after every exact
+  // one, by log2 volume then log2 flops (overflow fix).
+  struct Cost {
+    bool big = false;
+    double lvol = 0.0, lfl = 0.0;
+    std::int64_t vol = 0;
+    std::uint64_t fl = 0;
+  };
+  auto less = [](const Cost& x, const Cost& y) -> int {  // -1: x cheaper, 1: y cheaper, 0: tie
+    if (x.big != y.big) return x.big ? 1 : -1;
+    if (!x.big) return std::tie(x.vol, x.fl) < std::tie(y.vol, y.fl) ? -1 : (std::tie(y.vol, y.fl) < std::tie(x.vol, x.fl) ? 1 : 0);
+    return std::tie(x.lvol, x.lfl) < std::tie(y.lvol, y.lfl) ? -1 : (std::tie(y.lvol, y.lfl) < std::tie(x.lvol, x.lfl) ? 1 : 0);
+  };
   while (pool.size() > 1) {
     bool have = false;
-    std::int64_t best_vol = 0;
-    std::uint64_t best_flops = 0;
+    Cost best;
     std::pair<std::string, std::string> best_key;
     std::size_t bi = 0, bj = 0;
     for (std::size_t i = 0; i < pool.size(); ++i)
       for (std::size_t j = i + 1; j < pool.size(); ++j) {
         const TensorShape m = merge_free(pool[i].second, pool[j].second);
-        const std::int64_t vol = m.volume();
-        const std::uint64_t fl = flop_count(static_cast<std::uint64_t>(pool[i].second.volume()),
-                                            static_cast<std::uint64_t>(pool[j].second.volume()),
-                                            static_cast<std::uint64_t>(vol));
+        Cost c;
+        c.lvol = log2_volume(m);
+        const double la = log2_volume(pool[i].second), lb = log2_volume(pool[j].second);
+        c.lfl = 3.0 + 0.5 * (la + lb + c.lvol);
+        c.big = c.lvol >= 60.0 || la >= 60.0 || lb >= 60.0 || c.lfl >= 63.0;
+        if (!c.big) {
+          c.vol = m.volume();
+          c.fl = flop_count(static_cast<std::uint64_t>(pool[i].second.volume()),
+                            static_cast<std::uint64_t>(pool[j].second.volume()), static_cast<std::uint64_t>(c.vol));
+        }
         auto names = std::minmax(pool[i].first, pool[j].first);
         std::pair<std::string, std::string> key{names.first, names.second};
-        if (!have || std::tie(vol, fl, key) < std::tie(best_vol, best_flops, best_key)) {
+        const int cmp = have ? less(c, best) : -1;
+        if (cmp < 0 || (cmp == 0 && key < best_key)) {
           have = true;
-          best_vol = vol;
-          best_flops = fl;
+          best = c;
           best_key = key;
           bi = i;
           bj = j;
@@ -278,6 +313,20 @@ ContractionPlan greedy_plan(const NetworkShape& shape, const Cut& cut) {
   return p;
 }
 
+// For the budgeted cut search: a greedy plan whose sizes overflow (the
+// reference would wrap) counts as infinitely large instead of aborting the
+// search, so cuts can still bring it under the budget.
+ContractionPlan greedy_plan_or_huge(const NetworkShape& shape, const Cut& cut) {
+  try {
+    return greedy_plan(shape, cut);
+  } catch (const std::length_error&) {
+    ContractionPlan p;
+    p.cut = cut;
+    p.peak_memory = std::numeric_limits<std::int64_t>::max();
+    return p;
+  }
+}
+
 }  // namespace
 
 ContractionPlan plan_contraction(const NetworkShape& shape, const PlanOptions& opts) {
@@ -286,8 +335,9 @@ ContractionPlan plan_contraction(const NetworkShape& shape, const PlanOptions& o
     for (const auto& node : shape.nodes) biggest = std::max(biggest, node.bytes());
     if (opts.memory_budget < biggest) throw std::invalid_argument("memory budget below the largest node tensor");
   }
-  ContractionPlan plan = greedy_plan(shape, Cut{});
-  if (opts.memory_budget <= 0 || plan.peak_memory <= opts.memory_budget) return plan;
+  if (opts.memory_budget <= 0) return greedy_plan(shape, Cut{});
+  ContractionPlan plan = greedy_plan_or_huge(shape, Cut{});
+  if (plan.peak_memory <= opts.memory_budget) return plan;
 
   Cut cut;
   while (static_cast<int>(cut.labels.size()) < opts.max_cut_labels) {
@@ -300,7 +350,7 @@ ContractionPlan plan_contraction(const NetworkShape& shape, const PlanOptions& o
     for (const auto& l : candidates) {
       Cut trial = cut;
       trial.labels.push_back(l);
-      ContractionPlan p = greedy_plan(shape, trial);
+      ContractionPlan p = greedy_plan_or_huge(shape, trial);
       if (!found || p.peak_memory < best.peak_memory) {
         found = true;
         best = std::move(p);
@@ -319,7 +369,7 @@ ContractionPlan plan_contraction(const NetworkShape& shape, const PlanOptions& o
     // Each round multiplies the group by the last cut label's extent
     // (proj/src/plan.cpp:341-351).
     trial.group *= label_extent(shape, trial.labels.back());
-    ContractionPlan p = greedy_plan(shape, trial);
+    ContractionPlan p = greedy_plan_or_huge(shape, trial);
     if (p.peak_memory > opts.memory_budget) break;
     cut = trial;
     plan = std::move(p);

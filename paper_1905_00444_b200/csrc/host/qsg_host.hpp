@@ -159,6 +159,7 @@ struct PlanOptions {
 };
 
 std::uint64_t flop_count(std::uint64_t v0, std::uint64_t v1, std::uint64_t v2);
+double log2_volume(const TensorShape& t);  // sum of log2 extents (overflow-free size test)
 std::int64_t step_working_set(std::int64_t lhs_bytes, std::int64_t rhs_bytes, std::int64_t out_bytes);
 
 NetworkShape sliced_shape(const NetworkShape& s, const Cut& cut);

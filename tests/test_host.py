@@ -98,6 +98,16 @@ def test_greedy_planner_matches_reference():
         assert mine["per_slice"] == ref["per_slice"]
 
 
+def test_greedy_planner_rejects_overflow():
+    """the reference greedy wraps int64 volumes / uint64
+    flops on large grids (7x7 (1+32+1): 'rank 90, 1.6e14 flop').  Here the
+    candidate ordering stays defined past 2^60 and annotation refuses plans
+    whose sizes overflow, with the reference's error type for volume overflow."""
+    text = Q.generate_rqc(7, 7, 32, 0)
+    with pytest.raises(Q.LengthError, match="overflow"):
+        Q.plan_json(text, [0, 1], Q.PLAN_GREEDY)
+
+
 def test_fold_bit_exact(golden):
     for f in golden["folds"]:
         r, c, m, s = f["circuit"]
