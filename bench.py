@@ -58,6 +58,16 @@ def tc_split(step):
     return "3xFP16" if pair and (2 * step["k"]) % 32 == 0 else "3xTF32"
 
 
+def measured_traffic(kernel_name):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/r1_traffic.json), when it is the same launch."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)["kernels"].get(kernel_name)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -316,15 +326,22 @@ def run_ours(args):
     else:
         bound, peak_val, peak_note = "tensor", fp32_peak, (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x "
                                                            f"{smx:.0f} MHz ({peak_src} sm_max_mhz)")
+    kernel_name = (f"cgemm_tc ({split})" if top["tensor_cores"] else "cgemm_simt") + \
+        f" step s{top['step']:03d} m={top['m']} n={top['n']} k={top['k']}"
     perm_ms = sum(p["ms_total"] for p in perms)
     perm_bytes = sum(p["bytes"] * p["executions"] for p in perms)
     roof = {"bound": bound, "achieved": achieved, "peak": peak_val, "unit": "TFLOP/s", "frac": achieved / peak_val,
-            "traffic": None, "kernel": (f"cgemm_tc ({split})" if top["tensor_cores"] else "cgemm_simt") +
-            f" step s{top['step']:03d} m={top['m']} n={top['n']} k={top['k']}",
+            "traffic": None, "kernel": kernel_name,
             "kernel_share_of_step": top["ms_total"] / total_ms, "peak_source": peak_note,
             "fp32_simt_peak_tflops": fp32_peak,
             "permute_gbs": (perm_bytes / (perm_ms / 1e3) / 1e9) if perm_ms > 0 else None,
             "permute_share_of_step": perm_ms / total_ms, "hbm_peak_gbs": peaks["hbm_gbs"]}
+    traffic = measured_traffic(kernel_name)
+    if traffic is not None:
+        roof["traffic"] = traffic["dram_read_bytes"] + traffic["dram_write_bytes"]
+        roof["traffic_unit"] = "bytes per launch"
+        roof["traffic_source"] = traffic["report"]
+        roof["traffic_algorithmic"] = traffic["algorithmic_bytes"]
 
     line = None
     if rank == 0:
