@@ -144,6 +144,15 @@ enum { QSG_ENGINE_PROFILE = 1, QSG_ENGINE_NO_TENSOR_CORES = 2 };
  * kind 1, or `open` for kind 2), and compiles the device program. */
 int qsg_engine_create(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
                       int device, int flags, qsg_engine** out);
+/* As qsg_engine_create, with the reference's ExecOptions (include/qsim/
+ * engine.hpp:22-27): a contraction whose working set exceeds memory_budget
+ * bytes (0 = no limit) is decomposed into pieces (src/plan.cpp:355-472) and
+ * run through a pipeline of pipeline_depth pieces in flight
+ * (src/engine.cpp:52-180); its tensors live in pinned host memory and only
+ * the pieces occupy the device.  Error "indivisible contraction still over
+ * budget" (runtime error) as the reference. */
+int qsg_engine_create_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                         int device, int flags, int64_t memory_budget, int pipeline_depth, qsg_engine** out);
 int qsg_engine_destroy(qsg_engine* e);
 
 /* Compiles the device program for (circuit, plan) WITHOUT a device and
@@ -151,6 +160,9 @@ int qsg_engine_destroy(qsg_engine* e);
  * and CPU-side checks.  Arguments as qsg_engine_create. */
 int qsg_program_listing(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
                         int flags, char* buf, int64_t cap, int64_t* len);
+/* As qsg_program_listing with a memory budget (out-of-core placement). */
+int qsg_program_listing_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                           int flags, int64_t memory_budget, char* buf, int64_t cap, int64_t* len);
 
 typedef struct qsg_engine_info {
   int64_t num_qubits, num_slices, batch_size, num_steps, max_rank;

@@ -121,6 +121,8 @@ def lib():
                                fp, dp, P(u64), i32]),
         "qsg_normalize": (i32, [fp, i64, dp, P(i32)]),
         "qsg_engine_create": (i32, [cp, i32, cp, P(i32), i32, i32, i32, P(vp)]),
+        "qsg_engine_create_ex": (i32, [cp, i32, cp, P(i32), i32, i32, i32, i64, i32, P(vp)]),
+        "qsg_program_listing_ex": (i32, [cp, i32, cp, P(i32), i32, i32, i64, cp, i64, P(i64)]),
         "qsg_engine_destroy": (i32, [vp]),
         "qsg_program_listing": (i32, [cp, i32, cp, P(i32), i32, i32, cp, i64, P(i64)]),
         "qsg_engine_get_info": (i32, [vp, P(_EngineInfo)]),
@@ -334,11 +336,12 @@ def normalize_inplace(data: np.ndarray, log_scale: float = 0.0):
 
 
 def program_listing(circuit_text: str, plan_text: str = "", kind: int = PLAN_JSON, open_qubits=(),
-                    tensor_cores: bool = True) -> str:
-    """Device program the engine would run (no GPU needed): ops, GEMM shapes/paths, arena bytes."""
+                    tensor_cores: bool = True, memory_budget: int = 0) -> str:
+    """Device program the engine would run (no GPU needed): ops, GEMM shapes/paths, arena bytes;
+    with memory_budget > 0 the out-of-core placement (host arena, piece counts)."""
     a, p = _i32(open_qubits)
-    return _text(lib().qsg_program_listing, circuit_text.encode(), kind, plan_text.encode(), p, len(a),
-                 0 if tensor_cores else 2)
+    return _text(lib().qsg_program_listing_ex, circuit_text.encode(), kind, plan_text.encode(), p, len(a),
+                 0 if tensor_cores else 2, int(memory_budget))
 
 
 def xeb_score(n: int, probs, hog_median=None) -> dict:
@@ -377,12 +380,14 @@ class Engine:
     NO_TENSOR_CORES = 2
 
     def __init__(self, circuit_text: str, plan_text: str = "", kind: int = PLAN_JSON, open_qubits=(), device: int = 0,
-                 profile: bool = False, tensor_cores: bool = True):
+                 profile: bool = False, tensor_cores: bool = True, memory_budget: int = 0, pipeline_depth: int = 2):
+        """memory_budget / pipeline_depth: the reference's ExecOptions (include/qsim/engine.hpp:22-27) --
+        steps whose working set exceeds the budget run out of core (host-resident tensors, device pieces)."""
         self._h = C.c_void_p(0)
         a, p = _i32(open_qubits)
         flags = (self.PROFILE if profile else 0) | (0 if tensor_cores else self.NO_TENSOR_CORES)
-        _check(lib().qsg_engine_create(circuit_text.encode(), kind, plan_text.encode(), p, len(a), device, flags,
-                                       C.byref(self._h)))
+        _check(lib().qsg_engine_create_ex(circuit_text.encode(), kind, plan_text.encode(), p, len(a), device, flags,
+                                          int(memory_budget), int(pipeline_depth), C.byref(self._h)))
         info = _EngineInfo()
         _check(lib().qsg_engine_get_info(self._h, C.byref(info)))
         self.info = EngineInfo(*[getattr(info, f[0]) for f in _EngineInfo._fields_])

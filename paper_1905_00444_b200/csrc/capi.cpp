@@ -444,6 +444,39 @@ int qsg_engine_create(const char* circuit_text, int kind, const char* plan_text,
   });
 }
 
+int qsg_engine_create_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                         int device, int flags, int64_t memory_budget, int pipeline_depth, qsg_engine** out) {
+  return guarded([&] {
+    require_device();
+    if (memory_budget < 0 || pipeline_depth < 1) throw std::invalid_argument("engine: memory_budget >= 0, pipeline_depth >= 1");
+    const qsg::Circuit c = qsg::parse_circuit(circuit_text);
+    const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
+    qsg::EngineOptions o;
+    o.device = device;
+    o.profile = (flags & QSG_ENGINE_PROFILE) != 0;
+    o.tensor_cores = (flags & QSG_ENGINE_NO_TENSOR_CORES) == 0;
+    o.memory_budget = memory_budget;
+    o.pipeline_depth = pipeline_depth;
+    auto e = std::make_unique<qsg_engine>();
+    e->impl = std::make_unique<qsg::Engine>(c, plan, o);
+    *out = e.release();
+  });
+}
+
+int qsg_program_listing_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                           int flags, int64_t memory_budget, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    const qsg::Circuit c = qsg::parse_circuit(circuit_text);
+    const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
+    qsg::EngineOptions o;
+    o.compile_only = true;
+    o.tensor_cores = (flags & QSG_ENGINE_NO_TENSOR_CORES) == 0;
+    o.memory_budget = memory_budget;
+    qsg::Engine e(c, plan, o);
+    put_text(e.describe(), buf, cap, len);
+  });
+}
+
 int qsg_program_listing(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
                         int flags, char* buf, int64_t cap, int64_t* len) {
   return guarded([&] {

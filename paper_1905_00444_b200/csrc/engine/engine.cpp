@@ -99,6 +99,17 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
   op_execs_.assign(ops_.size(), 0);
   if (opt_.compile_only) return;  // program listing only (no device)
   check(cudaMalloc(&arena_, static_cast<std::size_t>(std::max<std::int64_t>(arena_bytes_, kAlign))), "arena cudaMalloc");
+  if (host_arena_bytes_ > 0) {
+    check(cudaHostAlloc(reinterpret_cast<void**>(&host_arena_), static_cast<std::size_t>(host_arena_bytes_),
+                        cudaHostAllocMapped | cudaHostAllocPortable),
+          "host arena cudaHostAlloc");
+    const int depth = std::max(1, opt_.pipeline_depth);
+    check(cudaMalloc(&ooc_scratch_, static_cast<std::size_t>(ooc_slot_bytes_) * static_cast<std::size_t>(depth)),
+          "out-of-core scratch cudaMalloc");
+    check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ooc_ev_.resize(2 * static_cast<std::size_t>(depth) + 2);
+    for (auto& e : ooc_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
   check(cudaMalloc(&metas_, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta cudaMalloc");
   check(cudaMemset(metas_, 0, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta memset");
   check(cudaMalloc(&acc_, sizeof(double2) * static_cast<std::size_t>(batch_)), "acc cudaMalloc");
@@ -131,6 +142,10 @@ Engine::~Engine() {
   if (stream_) cudaStreamSynchronize(stream_);
   for (auto e : ev_) cudaEventDestroy(e);
   if (arena_) cudaFree(arena_);
+  if (host_arena_) cudaFreeHost(host_arena_);
+  if (ooc_scratch_) cudaFree(ooc_scratch_);
+  for (auto e : ooc_ev_) cudaEventDestroy(e);
+  if (copy_stream_) cudaStreamDestroy(copy_stream_);
   if (metas_) cudaFree(metas_);
   if (acc_) cudaFree(acc_);
   if (per_slice_) cudaFree(per_slice_);
@@ -195,7 +210,7 @@ void Engine::compile() {
   };
   auto as_operand = [](const View& v) { return Operand{v.buf, v.off, v.node}; };
   // Emits K1 making `v` dense in `order`; returns the new view.
-  auto permute_to = [&](const View& v, const std::vector<Label>& order, int step) {
+  auto permute_to = [&](const View& v, const std::vector<Label>& order, int step, bool host = false) {
     Op op;
     op.kind = 0;
     op.step = step;
@@ -212,6 +227,7 @@ void Engine::compile() {
     op.count = out.volume();
     touch(v.buf);
     op.dst = new_buf(op.count * 8);
+    bufs_[static_cast<std::size_t>(op.dst)].host = host;
     out.buf = op.dst;
     out.off = 0;
     ops_.push_back(op);
@@ -325,17 +341,25 @@ void Engine::compile() {
       if (!X.has(l)) yfree.push_back(l);
     xfree = next_last(xfree);
     yfree = next_last(yfree);
+    // Out-of-core (ExecOptions::memory_budget semantics, src/engine.cpp:216-222):
+    // the step's working set exceeds the budget, or an operand already lives
+    // in host memory.  Its permuted operands and its result go to the
+    // pinned host arena; the GEMM runs as device pieces.
+    const std::int64_t xm = X.volume() / k, yn = Y.volume() / k;
+    const bool ooc = opt_.memory_budget > 0 &&
+                     (step_working_set(8 * xm * k, 8 * k * yn, 8 * xm * yn) > opt_.memory_budget ||
+                      bufs_[static_cast<std::size_t>(X.buf)].host || bufs_[static_cast<std::size_t>(Y.buf)].host);
     View A = X, B = Y;
     if (!best.use_a) {
       std::vector<Label> order = xfree;
       order.insert(order.end(), best.con.begin(), best.con.end());
-      A = permute_to(X, order, static_cast<int>(si));
+      A = permute_to(X, order, static_cast<int>(si), ooc);
       best.ta = false;
     }
     if (!best.use_b) {
       std::vector<Label> order = best.con;
       order.insert(order.end(), yfree.begin(), yfree.end());
-      B = permute_to(Y, order, static_cast<int>(si));
+      B = permute_to(Y, order, static_cast<int>(si), ooc);
       best.tb = false;
     }
     // Free-label orders as laid out in the operands.
@@ -365,7 +389,22 @@ void Engine::compile() {
     touch(A.buf);
     touch(B.buf);
     g.c = new_buf(g.m * g.n * 8);
-    if (g.ws_bytes > 0) g.ws = new_buf(g.ws_bytes);
+    g.ooc = ooc;
+    if (ooc) {
+      bufs_[static_cast<std::size_t>(g.c)].host = true;
+      g.tc = opt_.tensor_cores;  // decided per piece
+      g.ws_bytes = 0;
+      g.pieces = decompose_pieces(g.m, g.n, k, opt_.memory_budget);
+      for (const auto& pc : g.pieces) {
+        const std::int64_t ws = opt_.tensor_cores && dev::cgemm_tc_eligible(pc[1], pc[3], k, g.ta, g.tb)
+                                    ? dev::cgemm_tc_workspace_bytes(pc[1], pc[3], k, g.ta, g.tb)
+                                    : dev::cgemm_workspace_bytes(pc[1], pc[3], k);
+        ooc_slot_bytes_ = std::max(ooc_slot_bytes_, align_up(pc[1] * k * 8) + align_up(k * pc[3] * 8) +
+                                                        align_up(pc[1] * pc[3] * 8) + align_up(std::max<std::int64_t>(ws, 8)));
+      }
+    } else if (g.ws_bytes > 0) {
+      g.ws = new_buf(g.ws_bytes);
+    }
 
     // Output layout.  Natural GEMM order is [a_free, b_free]; when the
     // tcgen05 pair kernel runs, the epilogue can scatter C straight into
@@ -374,7 +413,7 @@ void Engine::compile() {
     // stay the three lowest output bits (64-byte store runs).
     std::vector<Label> out_order = a_free;
     out_order.insert(out_order.end(), b_free.begin(), b_free.end());
-    if (has_next && g.tc && dev::cgemm_tc_store_perm_supported(g.m, g.n, k, g.ta, g.tb) && a_free.size() <= 48 &&
+    if (has_next && !ooc && g.tc && dev::cgemm_tc_store_perm_supported(g.m, g.n, k, g.ta, g.tb) && a_free.size() <= 48 &&
         b_free.size() <= 24 && b_free.size() >= 3) {
       std::vector<Label> fr, cn;
       for (const auto& l : a_free) (next_con.count(l) ? cn : fr).push_back(l);
@@ -447,7 +486,7 @@ void Engine::split_handoffs() {
   const char* only = std::getenv("QSG_TC_CSPLIT_ONLY");  // debugging: restrict to one producer step
   for (std::size_t i = 0; i < ops_.size(); ++i) {
     Op& pr = ops_[i];
-    if (pr.kind != 1 || !pr.tc || !dev::cgemm_tc_split_ok(pr.m, pr.n, pr.k, pr.ta, pr.tb)) continue;
+    if (pr.kind != 1 || !pr.tc || pr.ooc || !dev::cgemm_tc_split_ok(pr.m, pr.n, pr.k, pr.ta, pr.tb)) continue;
     if (only && (std::string(",") + only + ",").find("," + std::to_string(pr.step) + ",") == std::string::npos) continue;
     int reader = -1, readers = 0;
     for (std::size_t j = i + 1; j < ops_.size(); ++j) {
@@ -460,7 +499,7 @@ void Engine::split_handoffs() {
     }
     if (readers != 1) continue;
     Op& co = ops_[static_cast<std::size_t>(reader)];
-    if (co.kind != 1 || !co.tc || co.a.buf != pr.c || co.b.buf == pr.c || co.a.off != 0 || co.a.node >= 0 || co.ta ||
+    if (co.kind != 1 || !co.tc || co.ooc || co.a.buf != pr.c || co.b.buf == pr.c || co.a.off != 0 || co.a.node >= 0 || co.ta ||
         co.m * co.k != pr.m * pr.n || co.meta_a != pr.meta_c || !dev::cgemm_tc_split_ok(co.m, co.n, co.k, co.ta, co.tb))
       continue;
     pr.c_split = true;
@@ -468,6 +507,111 @@ void Engine::split_handoffs() {
     co.ws_bytes = dev::cgemm_tc_workspace_bytes(co.m, co.n, co.k, co.ta, co.tb, true);
     if (co.ws >= 0) bufs_[static_cast<std::size_t>(co.ws)].bytes = align_up(std::max<std::int64_t>(co.ws_bytes, 8));
   }
+}
+
+// m / n blocks of an oversized contraction (src/plan.cpp:355-472 halves the
+// widest axis of the largest of m, n, k until the piece fits).  Pieces here
+// split only m and n: every output element keeps its whole K loop, so the
+// result is the in-core one (no partial-sum accumulation or renormalisation
+// of partial sums), and halving powers of two keeps pieces tensor-core shaped.
+std::vector<std::array<std::int64_t, 4>> Engine::decompose_pieces(std::int64_t m, std::int64_t n, std::int64_t k,
+                                                                   std::int64_t budget) {
+  std::vector<std::array<std::int64_t, 4>> out;
+  std::vector<std::array<std::int64_t, 4>> stack{{0, m, 0, n}};
+  while (!stack.empty()) {
+    const auto p = stack.back();
+    stack.pop_back();
+    if (step_working_set(8 * p[1] * k, 8 * k * p[3], 8 * p[1] * p[3]) <= budget) {
+      out.push_back(p);
+      continue;
+    }
+    const bool split_m = p[1] >= p[3] ? p[1] > 1 : p[3] <= 1;
+    if ((split_m && p[1] < 2) || (!split_m && p[3] < 2))
+      throw std::runtime_error("indivisible contraction still over budget");
+    const std::int64_t len = split_m ? p[1] : p[3], half = len / 2;
+    auto lo = p, hi = p;
+    (split_m ? lo[1] : lo[3]) = half;
+    (split_m ? hi[0] : hi[2]) += half;
+    (split_m ? hi[1] : hi[3]) = len - half;
+    stack.push_back(hi);  // the low half pops first (stable order)
+    stack.push_back(lo);
+  }
+  return out;
+}
+
+// Five-stage pipeline of one out-of-core GEMM (src/engine.cpp:52-180):
+// acquire a scratch slot, load the A row block and B column block
+// (host->device copies on the copy stream; 2-D copies for strided blocks),
+// execute on the engine stream, store the C block (device->host), release.
+// pipeline_depth slots are in flight, so loads and stores of neighbouring
+// pieces overlap the GEMM of the current one.
+void Engine::launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node_off, int* launches) {
+  const int depth = std::max(1, opt_.pipeline_depth);
+  const char* A = static_cast<const char*>(ptr(op.a, node_off));
+  const char* B = static_cast<const char*>(ptr(op.b, node_off));
+  char* C = base_of(op.c);
+  const std::int64_t k = op.k;
+  cudaEvent_t start = ooc_ev_[2 * static_cast<std::size_t>(depth)], done = ooc_ev_[2 * static_cast<std::size_t>(depth) + 1];
+  check(cudaEventRecord(start, stream_), "event");
+  check(cudaStreamWaitEvent(copy_stream_, start, 0), "wait");
+  for (std::size_t i = 0; i < op.pieces.size(); ++i) {
+    const auto& pc = op.pieces[i];
+    const std::int64_t m0 = pc[0], mp = pc[1], n0 = pc[2], np = pc[3];
+    const std::size_t slot = i % static_cast<std::size_t>(depth);
+    char* sA = ooc_scratch_ + static_cast<std::int64_t>(slot) * ooc_slot_bytes_;
+    char* sB = sA + align_up(mp * k * 8);
+    char* sC = sB + align_up(k * np * 8);
+    char* sW = sC + align_up(mp * np * 8);
+    cudaEvent_t loaded = ooc_ev_[2 * slot], computed = ooc_ev_[2 * slot + 1];
+    // load (copy stream, in order after the previous store of this slot)
+    if (!op.ta)
+      check(cudaMemcpyAsync(sA, A + m0 * k * 8, static_cast<std::size_t>(mp * k * 8), cudaMemcpyDefault, copy_stream_),
+            "ooc load A");
+    else
+      check(cudaMemcpy2DAsync(sA, static_cast<std::size_t>(mp * 8), A + m0 * 8, static_cast<std::size_t>(op.m * 8),
+                              static_cast<std::size_t>(mp * 8), static_cast<std::size_t>(k), cudaMemcpyDefault,
+                              copy_stream_),
+            "ooc load A");
+    if (op.tb)
+      check(cudaMemcpyAsync(sB, B + n0 * k * 8, static_cast<std::size_t>(np * k * 8), cudaMemcpyDefault, copy_stream_),
+            "ooc load B");
+    else
+      check(cudaMemcpy2DAsync(sB, static_cast<std::size_t>(np * 8), B + n0 * 8, static_cast<std::size_t>(op.n * 8),
+                              static_cast<std::size_t>(np * 8), static_cast<std::size_t>(k), cudaMemcpyDefault,
+                              copy_stream_),
+            "ooc load B");
+    check(cudaEventRecord(loaded, copy_stream_), "event");
+    // execute (engine stream)
+    check(cudaStreamWaitEvent(stream_, loaded, 0), "wait");
+    dev::GemmArgs g{};
+    g.a = sA;
+    g.b = sB;
+    g.c = sC;
+    g.m = mp;
+    g.n = np;
+    g.k = k;
+    g.trans_a = op.ta;
+    g.trans_b = op.tb;
+    g.meta_a = op.meta_a >= 0 ? metas_ + op.meta_a : nullptr;
+    g.meta_b = op.meta_b >= 0 ? metas_ + op.meta_b : nullptr;
+    g.norm_a = op.meta_a >= 0;
+    g.norm_b = op.meta_b >= 0;
+    g.meta_c = metas_ + op.meta_c;
+    g.workspace = sW;
+    const bool tc = op.tc && dev::cgemm_tc_eligible(mp, np, k, op.ta, op.tb);
+    g.workspace_bytes = tc ? dev::cgemm_tc_workspace_bytes(mp, np, k, op.ta, op.tb) : dev::cgemm_workspace_bytes(mp, np, k);
+    if (tc) check(dev::cgemm_tc(g, stream_, launches), "cgemm_tc");
+    else check(dev::cgemm(g, stream_, launches), "cgemm");
+    check(cudaEventRecord(computed, stream_), "event");
+    // store (copy stream)
+    check(cudaStreamWaitEvent(copy_stream_, computed, 0), "wait");
+    check(cudaMemcpy2DAsync(C + (m0 * op.n + n0) * 8, static_cast<std::size_t>(op.n * 8), sC,
+                            static_cast<std::size_t>(np * 8), static_cast<std::size_t>(np * 8),
+                            static_cast<std::size_t>(mp), cudaMemcpyDefault, copy_stream_),
+          "ooc store C");
+  }
+  check(cudaEventRecord(done, copy_stream_), "event");
+  check(cudaStreamWaitEvent(stream_, done, 0), "wait");
 }
 
 void Engine::pack_buffers() {
@@ -481,12 +625,13 @@ void Engine::pack_buffers() {
   });
   std::vector<int> placed;
   arena_bytes_ = 0;
+  host_arena_bytes_ = 0;
   for (int id : order) {
     Buffer& b = bufs_[static_cast<std::size_t>(id)];
     std::vector<std::pair<std::int64_t, std::int64_t>> busy;
     for (int p : placed) {
       const Buffer& o = bufs_[static_cast<std::size_t>(p)];
-      if (o.first <= b.last && b.first <= o.last) busy.emplace_back(o.offset, o.offset + o.bytes);
+      if (o.host == b.host && o.first <= b.last && b.first <= o.last) busy.emplace_back(o.offset, o.offset + o.bytes);
     }
     std::sort(busy.begin(), busy.end());
     std::int64_t off = 0;
@@ -495,15 +640,20 @@ void Engine::pack_buffers() {
       off = std::max(off, hi);
     }
     b.offset = off;
-    arena_bytes_ = std::max(arena_bytes_, off + b.bytes);
+    (b.host ? host_arena_bytes_ : arena_bytes_) = std::max(b.host ? host_arena_bytes_ : arena_bytes_, off + b.bytes);
     placed.push_back(id);
   }
+}
+
+char* Engine::base_of(int buf) const {
+  const Buffer& b = bufs_[static_cast<std::size_t>(buf)];
+  return (b.host ? host_arena_ : arena_) + b.offset;
 }
 
 void* Engine::ptr(const Operand& o, const std::vector<std::int64_t>& node_off) const {
   std::int64_t e = o.off;
   if (o.node >= 0) e += node_off[static_cast<std::size_t>(o.node)];
-  return arena_ + bufs_[static_cast<std::size_t>(o.buf)].offset + e * 8;
+  return base_of(o.buf) + e * 8;
 }
 
 std::int64_t Engine::prepare(const std::vector<int>& x1_bits) {
@@ -526,15 +676,16 @@ void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off,
   if (opt_.profile) check(cudaEventRecord(ev_[2 * i], stream_), "event");
   if (op.kind == 0) {
     const std::int64_t base = op.src.off + (op.src.node >= 0 ? node_off[static_cast<std::size_t>(op.src.node)] : 0);
-    check(dev::permute(arena_ + bufs_[static_cast<std::size_t>(op.src.buf)].offset, base,
-                       arena_ + bufs_[static_cast<std::size_t>(op.dst)].offset, static_cast<int>(op.ext.size()),
+    check(dev::permute(base_of(op.src.buf), base, base_of(op.dst), static_cast<int>(op.ext.size()),
                        op.ext.data(), op.istr.data(), stream_, &launches),
           "permute");
+  } else if (op.kind == 1 && op.ooc) {
+    launch_ooc_gemm(op, node_off, &launches);
   } else if (op.kind == 1) {
     dev::GemmArgs g{};
     g.a = ptr(op.a, node_off);
     g.b = ptr(op.b, node_off);
-    g.c = arena_ + bufs_[static_cast<std::size_t>(op.c)].offset;
+    g.c = base_of(op.c);
     g.m = op.m;
     g.n = op.n;
     g.k = op.k;
@@ -545,7 +696,7 @@ void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off,
     g.norm_a = op.meta_a >= 0;
     g.norm_b = op.meta_b >= 0;
     g.meta_c = metas_ + op.meta_c;
-    g.workspace = op.ws >= 0 ? arena_ + bufs_[static_cast<std::size_t>(op.ws)].offset : nullptr;
+    g.workspace = op.ws >= 0 ? base_of(op.ws) : nullptr;
     g.workspace_bytes = op.ws_bytes;
     g.store_perm = op.store_perm;
     g.c_split = op.c_split;
@@ -658,14 +809,19 @@ void Engine::reset_profile() {
 
 std::string Engine::describe() const {
   std::ostringstream os;
-  os << "arena " << arena_bytes_ << " B, nodes " << node_bytes_ << " B, ops " << ops_.size() << "\n";
+  os << "arena " << arena_bytes_ << " B, nodes " << node_bytes_ << " B, ops " << ops_.size();
+  if (host_arena_bytes_ > 0)
+    os << ", host arena " << host_arena_bytes_ << " B, pipeline scratch " << ooc_slot_bytes_ << " B x "
+       << std::max(1, opt_.pipeline_depth);
+  os << "\n";
   for (const auto& op : ops_) {
     if (op.kind == 0) os << "  permute step " << op.step << " elems " << op.count << " rank " << op.ext.size() << "\n";
     else if (op.kind == 1)
       os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << " flops " << op.flops
          << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes
          << (op.store_perm ? " fused-store" : "") << (op.c_split ? " split-out" : "")
-         << (op.a_presplit ? " split-in" : "") << "\n";
+         << (op.a_presplit ? " split-in" : "")
+         << (op.ooc ? " ooc pieces " + std::to_string(op.pieces.size()) : std::string()) << "\n";
     else os << "  accumulate " << op.count << "\n";
   }
   return os.str();

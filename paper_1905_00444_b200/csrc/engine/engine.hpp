@@ -40,6 +40,13 @@ struct EngineOptions {
   bool profile = false;     // CUDA events around every kernel op
   bool tensor_cores = true; // allow the tcgen05 GEMM for eligible steps
   bool compile_only = false; // build the program listing without touching a device
+  // Out-of-core execution (ExecOptions, include/qsim/engine.hpp:22-27): a
+  // contraction whose working set (in + out + max) exceeds memory_budget
+  // bytes runs as pieces (src/plan.cpp:355-472) through a device-side
+  // pipeline of depth pipeline_depth (src/engine.cpp:52-180); its operands
+  // and result live in pinned host memory.  0 = everything in HBM.
+  std::int64_t memory_budget = 0;
+  int pipeline_depth = 2;
 };
 
 struct OpProfile {
@@ -64,6 +71,7 @@ class Engine {
   const ContractionPlan& plan() const { return plan_; }
   std::int64_t batch_size() const { return batch_; }
   std::int64_t arena_bytes() const { return arena_bytes_; }
+  std::int64_t host_arena_bytes() const { return host_arena_bytes_; }
   std::int64_t node_bytes() const { return node_bytes_; }
   cudaStream_t stream() const { return stream_; }
   int device() const { return opt_.device; }
@@ -94,6 +102,7 @@ class Engine {
     std::int64_t bytes = 0;
     int first = 0, last = 0;
     std::int64_t offset = 0;
+    bool host = false;  // pinned host arena (out-of-core tensors)
   };
   struct Operand {
     int buf = -1;
@@ -122,13 +131,21 @@ class Engine {
     std::array<unsigned char, 24> col_pos{};
     bool c_split = false;     // C written as fp16 hi | lo planes (dev::GemmArgs::c_split)
     bool a_presplit = false;  // A read as fp16 hi | lo planes
+    // Out-of-core GEMM: m / n row-column blocks (m0, mp, n0, np) streamed
+    // through the device pipeline; C in host memory.
+    bool ooc = false;
+    std::vector<std::array<std::int64_t, 4>> pieces;
   };
 
   void compile();
   void split_handoffs();
   void pack_buffers();
   void* ptr(const Operand& o, const std::vector<std::int64_t>& node_off) const;
+  char* base_of(int buf) const;
+  static std::vector<std::array<std::int64_t, 4>> decompose_pieces(std::int64_t m, std::int64_t n, std::int64_t k,
+                                                                   std::int64_t budget);
   void launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot);
+  void launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node_off, int* launches);
 
   Circuit circuit_;
   ContractionPlan plan_;
@@ -150,6 +167,14 @@ class Engine {
   std::vector<Op> ops_;
   std::int64_t arena_bytes_ = 0;
   char* arena_ = nullptr;
+  // Out-of-core: pinned host arena (mapped) for oversized steps' tensors,
+  // device scratch slots for their pieces, the copy stream and its events.
+  std::int64_t host_arena_bytes_ = 0;
+  char* host_arena_ = nullptr;
+  std::int64_t ooc_slot_bytes_ = 0;
+  char* ooc_scratch_ = nullptr;
+  cudaStream_t copy_stream_ = nullptr;
+  std::vector<cudaEvent_t> ooc_ev_;
   dev::TMeta* metas_ = nullptr;
   int nmeta_ = 0;
   double2* acc_ = nullptr;

@@ -214,3 +214,64 @@ def test_tensor_core_paths_forced_small_vs_oracle(gpu, monkeypatch):
     with gpu.Engine(text, plan, tensor_cores=False) as e:
         _, samps = e.amplitude_batch(x1, [0, 1])
     assert rel(amps, samps) < 1e-5
+
+
+def _small_config2_like(gpu, depth=20):
+    text = gpu.generate_rqc(7, 7, depth, 0)
+    order = json.load(open(os.path.join(ROOT, "configs", "config2_plan.json")))["order"]
+    opn = [32, 33, 34, 39, 40, 41, 45, 46, 47, 48]
+    plan = json.dumps({"version": 1, "open_qubits": opn, "cut": {"labels": ["b_007_003_004"], "group": 1},
+                       "order": order})
+    return text, plan, opn
+
+
+@pytest.mark.parametrize("tc", [True, False])
+def test_out_of_core_matches_in_core(gpu, tc):
+    """SURVEY 8f row 1 (ExecOptions::memory_budget, src/engine.cpp:216-222):
+    steps whose working set exceeds the budget run as m/n pieces through the
+    depth-2 copy/compute pipeline with their tensors in pinned host memory;
+    the amplitudes equal the in-HBM run (every output element keeps its full
+    K loop), the device arena shrinks, and the oracle agrees."""
+    import qsim_oracle as O
+    text, plan, opn = _small_config2_like(gpu)
+    budget = 1 << 20  # 31 of 48 steps out of core, 231 pieces
+    listing = gpu.program_listing(text, plan, tensor_cores=tc, memory_budget=budget)
+    head = listing.splitlines()[0]
+    assert "host arena" in head and listing.count(" ooc pieces ") >= 5
+    full = int(gpu.program_listing(text, plan, tensor_cores=tc).splitlines()[0].split()[1])
+    assert int(head.split()[1]) < full
+    x1 = gpu.draw_x1(49, opn, 5, 0)
+    with gpu.Engine(text, plan, tensor_cores=tc) as e:
+        _, ref = e.amplitude_batch(x1, [0, 1])
+    for depth in (1, 2, 3):
+        with gpu.Engine(text, plan, tensor_cores=tc, memory_budget=budget, pipeline_depth=depth) as e:
+            bits, amps = e.amplitude_batch(x1, [0, 1])
+        assert rel(amps, ref) < 1e-6, depth
+    obits, oamps = O.amplitude_batch(text, plan, x1, [0, 1])
+    assert bits == obits and rel(amps, oamps) < 1e-5
+
+
+def test_out_of_core_config2_full_size(gpu):
+    """Config 2 at full size under an 8 GiB contraction budget: 18 of 48
+    steps (including s026, whose operands alone are 17 GiB) run out of core
+    with ~36 GB of tensors in host memory; amplitudes match the in-HBM run."""
+    text = gpu.generate_rqc(7, 7, 32, 0)
+    plan = open(os.path.join(ROOT, "configs", "config2_plan.json")).read()
+    x1 = gpu.draw_x1(49, json.loads(plan)["open_qubits"], 0, 2)
+    with gpu.Engine(text, plan) as e:
+        e.prepare(x1)
+        e.run([0], reset=True)
+        ref = e.results()
+    with gpu.Engine(text, plan, memory_budget=8 << 30) as e:
+        assert "ooc" in e.describe()
+        e.prepare(x1)
+        e.run([0], reset=True)
+        got = e.results()
+    assert rel(got, ref) < 1e-6
+
+
+def test_out_of_core_indivisible(gpu):
+    """The reference's error when no piece fits (src/plan.cpp:437)."""
+    text, plan, _ = _small_config2_like(gpu, depth=12)
+    with pytest.raises(gpu.QsgError, match="indivisible contraction still over budget"):
+        gpu.Engine(text, plan, memory_budget=64)

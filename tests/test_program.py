@@ -36,3 +36,21 @@ def test_heavy_steps_on_tensor_cores_and_arena_fits(cfg, shape):
 def test_no_tensor_core_program_uses_simt_everywhere():
     plan, lines = listing("config2", 7, 7, 32, 0, tensor_cores=False)
     assert all("simt" in l.split() for l in lines if l.split()[0] == "gemm")
+
+
+def test_out_of_core_placement():
+    """memory_budget (ExecOptions): oversized steps and every step reading
+    their host-resident results go out of core; the device arena shrinks to
+    what the in-core steps need, the rest is the pinned host arena."""
+    text = Q.generate_rqc(7, 7, 32, 0)
+    plan = open(os.path.join(ROOT, "configs", "config2_plan.json")).read()
+    full = Q.program_listing(text, plan).splitlines()
+    lines = Q.program_listing(text, plan, memory_budget=8 << 30).splitlines()
+    head = lines[0].split()
+    assert int(head[1]) < 0.2 * int(full[0].split()[1])
+    assert "host" in lines[0]
+    ooc = [l.split() for l in lines if " ooc pieces " in l]
+    assert any(f[2] == "26" and int(f[-1]) >= 2 for f in ooc)  # s026 (17 GiB of operands) is split
+    assert sum(int(f[10]) for f in (l.split() for l in lines) if f[0] == "gemm") == json.loads(plan)["per_slice"]["flops"]
+    with pytest.raises(Q.QsgError, match="indivisible"):
+        Q.program_listing(text, plan, memory_budget=4096)
