@@ -220,7 +220,7 @@ def run_ours(args):
     plan = json.loads(plan_text)
     open_q = plan["open_qubits"]
     n = r * c
-    eng = Q.Engine(text, plan_text, device=local, tensor_cores=not args.no_tc)
+    eng = Q.Engine(text, plan_text, device=local, tensor_cores=not args.no_tc, memory_budget=args.memory_budget)
     info = eng.info
     K = plan["slices"]
     per_step = cfg["slices_per_step"] or K
@@ -354,7 +354,8 @@ def run_ours(args):
                        "amplitudes_per_step_per_gpu": batch, "slices_per_step_per_gpu": per_step,
                        "flops_per_step_per_gpu": info.flops_per_slice * per_step,
                        "l2": "intermediates (up to 16 GiB) >> 126 MB L2; no flush needed",
-                       "arena_bytes": info.arena_bytes, "tensor_cores": not args.no_tc},
+                       "arena_bytes": info.arena_bytes, "tensor_cores": not args.no_tc,
+                       **({"memory_budget": args.memory_budget} if args.memory_budget else {})},
             "tflops_eq1": tflops, "tflops_frac_fp32_simt": tflops / fp32_peak,
             "e2e": {"value": e2e_value, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "note": f"host x1 per step selects resident node views (open fold uploaded once per circuit, "
@@ -400,6 +401,8 @@ def main():
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-out", default="", help="write the per-op profile (one JSON line per op) here")
+    ap.add_argument("--memory-budget", type=int, default=0,
+                    help="bytes per contraction (reference ExecOptions); larger steps run out of core")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--cpu-budget-flops", type=float, default=4e11,
                     help="Eq.1 flops per task of the reference CPU sample (plan prefix)")
