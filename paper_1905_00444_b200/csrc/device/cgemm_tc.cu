@@ -1534,7 +1534,15 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.meta_c = g.meta_c;
   p.norm_a = g.norm_a && g.meta_a != nullptr;
   p.norm_b = g.norm_b && g.meta_b != nullptr;
-  p.chunk = std::max(1, chunk_blocks() / 2);  // promotion interval in real K stays 128
+  // Promotion interval: 128 real K (2 k-blocks; relative error ~1e-6,
+  // linear in the interval, tests/tc_accuracy).  Short-K tiles (k <= 256)
+  // use 2 chunks of k/2: every promotion is a TMEM hand-off between the MMA
+  // and the worker warps that also write the tile epilogue, and with 4 per
+  // 8-k-block tile the MMA waits on them (measured: the k = 256 steps of
+  // config 2 run 25-35% faster; error ~2e-6).
+  const char* chunk_env = std::getenv("QSG_TC_CHUNK");
+  if (chunk_env) p.chunk = std::max(1, chunk_blocks() / 2);
+  else p.chunk = p.kblocks <= 8 ? std::max(2, (p.kblocks + 1) / 2) : 2;
   p.store_perm = g.store_perm ? 1 : 0;
   p.nrow_bits = g.nrow_bits;
   p.ncol_bits = g.ncol_bits;
