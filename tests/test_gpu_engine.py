@@ -171,6 +171,28 @@ def test_config2_full_size_tensor_core_vs_simt(gpu):
     assert 0.8 < np.mean(np.abs(a) ** 2) * 2.0**49 < 1.25
 
 
+def test_config5_slice_tensor_core_vs_simt(gpu):
+    """Config 5 (7x7, 1+40+1, reference_plan_7x7) at full size, one slice
+    (7.2e14 flop, rank-30 intermediates, 2^15 x 2^15 x 2^15 GEMMs): the
+    tcgen05 3xFP16 engine (split hand-offs, pre-split A, K-sync) vs the
+    FP32-FFMA engine -- north-star tolerance on |amp| and fidelity."""
+    text = gpu.generate_rqc(7, 7, 40, 0)
+    plan = open(os.path.join(ROOT, "configs", "config5_plan.json")).read()
+    x1 = gpu.draw_x1(49, json.loads(plan)["open_qubits"], 0, 0)
+    res = {}
+    for tc in (True, False):
+        with gpu.Engine(text, plan, tensor_cores=tc) as e:
+            e.prepare(x1)
+            e.run([5], reset=True)
+            res[tc] = e.results()
+    a, b = res[True], res[False]
+    big = np.abs(b) > 0.1 * np.abs(b).mean()
+    assert np.max(np.abs(np.abs(a[big]) - np.abs(b[big])) / np.abs(b[big])) < 1e-4
+    fid = abs(np.vdot(a, b)) ** 2 / (np.vdot(a, a).real * np.vdot(b, b).real)
+    assert fid >= 1 - 1e-6
+    assert rel(a, b) < 1e-4
+
+
 def test_split_handoffs_match_fp32_storage(gpu, monkeypatch):
     """GEMM -> GEMM hand-offs in fp16 hi|lo split storage (config 2 has 13
     chained ones, up to five in a row): same amplitudes as fp32 storage to
