@@ -104,7 +104,6 @@ struct TcParams {
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
   unsigned char col_pos[24];
-  int raw_hi;  // experiment: feed raw fp32 as the hi part (valid iff the tensor core truncates)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -186,8 +185,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-
-__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t u;
@@ -330,18 +327,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int idx = i * kWorkers + wt;
             const float4 x = a[idx];
             float4 h, l;
-            if (p.raw_hi) {
-              l.x = x.x - tf32_trunc(x.x);
-              l.y = x.y - tf32_trunc(x.y);
-              l.z = x.z - tf32_trunc(x.z);
-              l.w = x.w - tf32_trunc(x.w);
-            } else {
-              h.x = tf32_rna(x.x); l.x = x.x - h.x;
-              h.y = tf32_rna(x.y); l.y = x.y - h.y;
-              h.z = tf32_rna(x.z); l.z = x.z - h.z;
-              h.w = tf32_rna(x.w); l.w = x.w - h.w;
-              a[idx] = h;
-            }
+            h.x = tf32_rna(x.x); l.x = x.x - h.x;
+            h.y = tf32_rna(x.y); l.y = x.y - h.y;
+            h.z = tf32_rna(x.z); l.z = x.z - h.z;
+            h.w = tf32_rna(x.w); l.w = x.w - h.w;
+            a[idx] = h;
             alo[idx] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -636,18 +626,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int idx = i * kWorkers + wt;
             const float4 x = a[idx];
             float4 h, l;
-            if (p.raw_hi) {
-              l.x = x.x - tf32_trunc(x.x);
-              l.y = x.y - tf32_trunc(x.y);
-              l.z = x.z - tf32_trunc(x.z);
-              l.w = x.w - tf32_trunc(x.w);
-            } else {
-              h.x = tf32_rna(x.x); l.x = x.x - h.x;
-              h.y = tf32_rna(x.y); l.y = x.y - h.y;
-              h.z = tf32_rna(x.z); l.z = x.z - h.z;
-              h.w = tf32_rna(x.w); l.w = x.w - h.w;
-              a[idx] = h;
-            }
+            h.x = tf32_rna(x.x); l.x = x.x - h.x;
+            h.y = tf32_rna(x.y); l.y = x.y - h.y;
+            h.z = tf32_rna(x.z); l.z = x.z - h.z;
+            h.w = tf32_rna(x.w); l.w = x.w - h.w;
+            a[idx] = h;
             alo[idx] = l;
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1269,8 +1252,7 @@ __global__ void __launch_bounds__(256) tc_prep_b_f16_kernel(const float2* __rest
 
 // B (complex, [k][n] or [n][k]) -> B_r^T hi/lo planes [2n][2k] fp32.
 __global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict__ b, float* __restrict__ hi,
-                                                        float* __restrict__ lo, long long n, long long k, int tb,
-                                                        int raw_hi) {
+                                                        float* __restrict__ lo, long long n, long long k, int tb) {
   __shared__ float2 tile[32][33];  // [p_local][j_local]
   const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -1290,24 +1272,10 @@ __global__ void __launch_bounds__(256) tc_prep_b_kernel(const float2* __restrict
     if (j >= n || p >= k) continue;
     const float2 v = tile[tx][r];
     const float re = v.x, im = v.y;
-    float h0, h1, h2, h3;
-    uint32_t u;
-    if (raw_hi) {
-      h0 = tf32_trunc(re); h1 = tf32_trunc(-im); h2 = tf32_trunc(im);
-    } else {
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(re)); h0 = __uint_as_float(u);
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(-im)); h1 = __uint_as_float(u);
-      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(im)); h2 = __uint_as_float(u);
-    }
-    h3 = h0;
+    const float h0 = tf32_rna(re), h1 = tf32_rna(-im), h2 = tf32_rna(im), h3 = h0;
     const long long row0 = (2 * j) * k2 + 2 * p, row1 = (2 * j + 1) * k2 + 2 * p;
-    if (raw_hi) {
-      *reinterpret_cast<float2*>(hi + row0) = make_float2(re, -im);
-      *reinterpret_cast<float2*>(hi + row1) = make_float2(im, re);
-    } else {
-      *reinterpret_cast<float2*>(hi + row0) = make_float2(h0, h1);
-      *reinterpret_cast<float2*>(hi + row1) = make_float2(h2, h3);
-    }
+    *reinterpret_cast<float2*>(hi + row0) = make_float2(h0, h1);
+    *reinterpret_cast<float2*>(hi + row1) = make_float2(h2, h3);
     *reinterpret_cast<float2*>(lo + row0) = make_float2(re - h0, -im - h1);
     *reinterpret_cast<float2*>(lo + row1) = make_float2(im - h2, re - h3);
   }
@@ -1388,11 +1356,6 @@ int chunk_blocks() {
   return v >= 1 ? v : kChunkDefault;
 }
 
-bool raw_hi_mode() {
-  const char* env = std::getenv("QSG_TC_RAWHI");
-  return env && env[0] == '1';
-}
-
 // Persistent grid: one CTA pair per SM pair (74 on a 148-SM B200).
 long long pair_slots() {
   static long long n = [] {
@@ -1449,7 +1412,6 @@ cudaError_t launch_pair(const GemmArgs& g, const float* bhi, const float* blo, c
   p.meta_c = g.meta_c;
   p.norm_a = g.norm_a;
   p.norm_b = g.norm_b;
-  p.raw_hi = raw_hi_mode() ? 1 : 0;
   p.chunk = chunk_blocks();
   p.store_perm = g.store_perm ? 1 : 0;
   p.nrow_bits = g.nrow_bits;
@@ -1704,8 +1666,7 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
   float* blo = bhi + (2 * g.n) * (2 * g.k);
   {
     dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
-    tc_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k, g.trans_b ? 1 : 0,
-                                                raw_hi_mode() ? 1 : 0);
+    tc_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), bhi, blo, g.n, g.k, g.trans_b ? 1 : 0);
     if (launches) ++*launches;
   }
   if (g.store_perm && !use_pair(g.m, g.n))
@@ -1735,7 +1696,6 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
   p.meta_c = g.meta_c;
   p.norm_a = g.norm_a;
   p.norm_b = g.norm_b;
-  p.raw_hi = raw_hi_mode() ? 1 : 0;
   p.chunk = chunk_blocks();
   const long long mt = g.m / BM, nt = (2 * g.n) / bn;
   if (mt * nt > 2147483647LL || g.m > 2147483647LL) throw std::length_error("cgemm_tc: too many tiles");
