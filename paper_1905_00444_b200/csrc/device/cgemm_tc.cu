@@ -912,21 +912,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         pair_tile_coords(cluster + ti * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
         const int row0 = static_cast<int>(m_pair * 256 + static_cast<long long>(rank) * BM);
         const int brow0 = n_tile * kPairBN + static_cast<int>(rank) * (kPairBN / 2);
-        // K-sync: the producers of one wave of tiles stay within two
-        // checkpoints of each other, so the A / B k-slabs they share are
-        // still in L2 when the last of them reads it (unsynchronised
-        // pairs drift apart by more than L2 holds and re-stream from HBM).
-        const int ncheck = kblocks / max(p.sync_every, 1) + 1;
-        const unsigned need = 2u * static_cast<unsigned>(min(nclusters, total - ti * nclusters));
-        unsigned int* ctr = p.sync ? p.sync + ti * ncheck : nullptr;
+        // K-sync: the producers stay within two checkpoints of each other,
+        // counted in k-blocks over the whole persistent run (tile ti of
+        // every pair belongs to the same wave), so the A / B k-slabs that
+        // concurrently running pairs share are still in L2 when the last of
+        // them reads them.  Unsynchronised pairs drift apart by more than L2
+        // holds and re-stream from HBM (long-K tiles: within a tile; short-K
+        // tiles: across tiles).
+        const long long gk0 = ti * kblocks;
         for (int kb = 0; kb < kblocks; ++kb) {
-          if (ctr && kb % p.sync_every == 0) {
-            const int c = kb / p.sync_every;
-            atomicAdd(ctr + c, 1u);
+          const long long gk = gk0 + kb;
+          if (p.sync && gk % p.sync_every == 0) {
+            const long long c = gk / p.sync_every;
+            atomicAdd(p.sync + c, 1u);
             if (c >= 1) {
+              // pairs whose run reaches k-block (c-1)*every: all with base
+              // tiles if it falls inside those, else the `extra` ones.
+              const long long kprev = (c - 1) * p.sync_every;
+              const long long base = total / nclusters, extra = total % nclusters;
+              const long long have = kprev < base * kblocks ? min(nclusters, total)
+                                     : (kprev < (base + 1) * kblocks ? extra : 0);
+              const unsigned need = 2u * static_cast<unsigned>(have);
               for (int spin = 0; spin < 4096; ++spin) {  // bounded: never a deadlock, at worst unsynchronised
                 unsigned v;
-                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr + c - 1) : "memory");
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync + c - 1) : "memory");
                 if (v >= need) break;
                 __nanosleep(128);
               }
@@ -1443,14 +1452,14 @@ int sync_every() {
   return env ? std::max(0, std::atoi(env)) : 16;
 }
 
-// Counters for every (wave, checkpoint); waves <= tiles.  0 when K-sync is
-// off or the K loop is too short to drift.
+// Counters for every checkpoint of the longest per-pair run (at most all
+// tiles on one pair); 0 when K-sync is off.
 std::int64_t sync_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   const int every = sync_every();
   const std::int64_t kblocks = (2 * k + BK16 - 1) / BK16;
-  if (every <= 0 || kblocks < 4 * every || !use_pair(m, n)) return 0;
+  if (every <= 0 || !use_pair(m, n)) return 0;
   const std::int64_t tiles = (m / 256) * ((2 * n) / pair_bn(n));
-  return ((tiles * (kblocks / every + 1) * 4 + 255) / 256) * 256;
+  return ((((tiles * kblocks) / every + 2) * 4 + 255) / 256) * 256;  // checkpoints of the longest run (1 pair)
 }
 
 // Pre-split A: a streaming pass converts A to fp16 hi / lo planes so the
