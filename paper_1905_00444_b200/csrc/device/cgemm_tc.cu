@@ -759,11 +759,11 @@ __device__ __forceinline__ int max_exp(const TMeta* m) {
 
 // K-major, SWIZZLE_64B descriptor (rows of 64 B, 8-row atoms of 512 B at a
 // 1 KiB stride: the hi and lo atoms of one 8-row group are interleaved).
-__device__ __forceinline__ uint64_t kmajor_sw64_desc(uint32_t saddr) {
+__device__ __forceinline__ uint64_t kmajor_sw64_desc(uint32_t saddr, uint32_t sbo) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
   d |= static_cast<uint64_t>(1) << 16;
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO
+  d |= static_cast<uint64_t>(sbo >> 4) << 32;  // stride between 8-row atoms
   d |= static_cast<uint64_t>(1) << 46;
   d |= static_cast<uint64_t>(4) << 61;           // SWIZZLE_64B
   return d;
@@ -824,10 +824,10 @@ __device__ __forceinline__ void split_f16x8(const float4& a, const float4& b, fl
   lo = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
-template <int BN>
+template <int BN, int KB = BK16>
 struct Tc5Cfg {
-  static constexpr int A_B = BM * BK16 * 4;        // raw fp32 A tile = hi0|lo0|hi1|lo1 after conversion
-  static constexpr int B_B = (BN / 2) * BK16 * 2;  // one fp16 plane of this CTA's half of B_r^T
+  static constexpr int A_B = BM * KB * 4;        // raw fp32 A tile (= A hi + lo fp16 planes)
+  static constexpr int B_B = (BN / 2) * KB * 2;  // one fp16 plane of this CTA's half of B_r^T
   static constexpr int STAGE_BYTES = A_B + 2 * B_B;
   static constexpr int EPI_PITCH = 20;
   static constexpr int EPI_BYTES = (kWorkers / 32) * 32 * EPI_PITCH * 4;
@@ -842,13 +842,15 @@ struct Tc5Cfg {
 // a producer epilogue), so the stage is TMA -> MMA with no worker pass:
 // both CTAs' TMA loads complete on the leader's full[s] (cta_group::2) and
 // the worker warps only promote and store.  map_a is then the A_hi plane
-// and map_alo the A_lo plane (SW128, 64 fp16 per row).
-template <int kPairBN, bool kSplitA>
+// and map_alo the A_lo plane (64 or 32 fp16 per row per stage: SW128 or SW64).
+template <int kPairBN, bool kSplitA, int kBK = BK16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_alo,
                           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
                           const TcParams p) {
-  using Cfg = Tc5Cfg<kPairBN>;
+  using Cfg = Tc5Cfg<kPairBN, kBK>;
+  static_assert(kSplitA || kBK == kBK, "in-kernel A conversion uses 64-K stages");
+  static_assert(kBK == 64 || kBK == 32, "stage K");
   constexpr int HALF = kPairBN / 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KiB aligned, still __shared__
@@ -948,19 +950,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t bar = smem_u32(&full[s]);
             if (rank == 0) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
             else asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(bar) : "r"(bar));
-            tma_load_2d_pair(&map_a, bar, st, kb * BK16, row0);
-            tma_load_2d_pair(&map_alo, bar, st + Cfg::A_B / 2, kb * BK16, row0);
-            tma_load_2d_pair(&map_bhi, bar, st + Cfg::A_B, kb * BK16, brow0);
-            tma_load_2d_pair(&map_blo, bar, st + Cfg::A_B + Cfg::B_B, kb * BK16, brow0);
+            tma_load_2d_pair(&map_a, bar, st, kb * kBK, row0);
+            tma_load_2d_pair(&map_alo, bar, st + Cfg::A_B / 2, kb * kBK, row0);
+            tma_load_2d_pair(&map_bhi, bar, st + Cfg::A_B, kb * kBK, brow0);
+            tma_load_2d_pair(&map_blo, bar, st + Cfg::A_B + Cfg::B_B, kb * kBK, brow0);
             if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
             continue;
           }
           const bool tail = p.half_tail && kb == kblocks - 1;
           mbar_expect_tx(&full[s], tail ? Cfg::STAGE_BYTES - Cfg::A_B / 2 : Cfg::STAGE_BYTES);
-          tma_load_2d(&map_a, &full[s], st, kb * BK16, row0);
-          if (!tail) tma_load_2d(&map_a, &full[s], st + Cfg::A_B / 2, kb * BK16 + BK16 / 2, row0);
-          tma_load_2d(&map_bhi, &full[s], st + Cfg::A_B, kb * BK16, brow0);
-          tma_load_2d(&map_blo, &full[s], st + Cfg::A_B + Cfg::B_B, kb * BK16, brow0);
+          tma_load_2d(&map_a, &full[s], st, kb * kBK, row0);
+          if (!tail) tma_load_2d(&map_a, &full[s], st + Cfg::A_B / 2, kb * kBK + kBK / 2, row0);
+          tma_load_2d(&map_bhi, &full[s], st + Cfg::A_B, kb * kBK, brow0);
+          tma_load_2d(&map_blo, &full[s], st + Cfg::A_B + Cfg::B_B, kb * kBK, brow0);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -984,18 +986,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           else mbar_wait_cluster(&conv[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
-          const uint64_t b_hi = kmajor_sw128_desc(st + Cfg::A_B);
-          const uint64_t b_lo = kmajor_sw128_desc(st + Cfg::A_B + Cfg::B_B);
-          const uint64_t a0 = kmajor_sw64_desc(st);
+          // 64-K stages: SW128 planes (128-byte rows); 32-K stages: SW64 (64-byte rows, 512-byte atoms)
+          const uint64_t b_hi = kBK == 64 ? kmajor_sw128_desc(st + Cfg::A_B) : kmajor_sw64_desc(st + Cfg::A_B, 512);
+          const uint64_t b_lo = kBK == 64 ? kmajor_sw128_desc(st + Cfg::A_B + Cfg::B_B)
+                                          : kmajor_sw64_desc(st + Cfg::A_B + Cfg::B_B, 512);
+          const uint64_t a0 = kmajor_sw64_desc(st, 1024);
           const bool first = kb == c * p.chunk;
-          const int nkk = (p.half_tail && kb == kblocks - 1) ? 2 : BK16 / 16;  // zero-filled B half not needed
+          const int nkk = (p.half_tail && kb == kblocks - 1) ? 2 : kBK / 16;  // zero-filled B half not needed
 #pragma unroll
-          for (int kk = 0; kk < BK16 / 16; ++kk) {
+          for (int kk = 0; kk < kBK / 16; ++kk) {
             if (kk == nkk) break;
             uint64_t a_hi, a_lo;
-            if constexpr (kSplitA) {  // SW128 planes: +32 B per K=16 step
-              a_hi = kmajor_sw128_desc(st) + static_cast<uint64_t>(kk * 2);
-              a_lo = kmajor_sw128_desc(st + Cfg::A_B / 2) + static_cast<uint64_t>(kk * 2);
+            if constexpr (kSplitA) {  // +32 B per K=16 step
+              a_hi = (kBK == 64 ? kmajor_sw128_desc(st) : kmajor_sw64_desc(st, 512)) + static_cast<uint64_t>(kk * 2);
+              a_lo = (kBK == 64 ? kmajor_sw128_desc(st + Cfg::A_B / 2) : kmajor_sw64_desc(st + Cfg::A_B / 2, 512)) +
+                     static_cast<uint64_t>(kk * 2);
             } else {
               a_hi = a0 + static_cast<uint64_t>(((kk >> 1) * (Cfg::A_B / 2) + (kk & 1) * 32) >> 4);
               a_lo = a_hi + (512 >> 4);
@@ -1339,15 +1344,18 @@ long long b16_pitch(std::int64_t k) {
   return 2 * k + (env ? std::atoll(env) : 0);
 }
 
-// fp16 map: inner dim `cols` (contiguous), box [box_rows x 64] (128 B), SW128.
-CUtensorMap make_map_f16(const void* base, long long cols, long long rows, long long pitch, int box_rows) {
+// fp16 map: inner dim `cols` (contiguous), box [box_rows x kb] with kb = 64
+// (128 B rows, SW128) or 32 (64 B rows, SW64).
+CUtensorMap make_map_f16(const void* base, long long cols, long long rows, long long pitch, int box_rows,
+                         int kb = BK16) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch) * 2};
-  const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK16), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(kb), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, l2_promo(),
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
@@ -1481,16 +1489,19 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                             const __half* blo, unsigned int* sync, const __half* ahi, const __half* alo,
                             cudaStream_t stream) {
   const bool split = ahi != nullptr;
-  const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM) : make_map(g.a, 2 * g.k, g.m, BM);
-  const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM) : ma;
-  const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2);
-  const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2);
+  // Pre-split A: pure TMA -> MMA stages; 32-K stages (6 in flight instead
+  // of 3) hide more HBM latency where A streams from DRAM (QSG_TC_KB).
+  const int kb = split && (2 * g.k) % 32 == 0 ? (env_int("QSG_TC_KB", 64) == 32 ? 32 : 64) : BK16;
+  const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM, kb) : make_map(g.a, 2 * g.k, g.m, BM);
+  const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM, kb) : ma;
+  const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
+  const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
   TcParams p{};
   p.c = static_cast<float*>(g.c);
   p.m = g.m;
   p.n2 = 2 * g.n;
-  p.kblocks = static_cast<int>((2 * g.k + BK16 - 1) / BK16);
-  p.half_tail = (2 * g.k) % BK16 != 0 ? 1 : 0;
+  p.kblocks = static_cast<int>((2 * g.k + kb - 1) / kb);
+  p.half_tail = (2 * g.k) % kb != 0 ? 1 : 0;
   p.group_m = env_int("QSG_TC_GROUPM", kGroupM);
   p.sync = sync;
   p.sync_every = sync_every();
@@ -1512,8 +1523,9 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   // 8-k-block tile the MMA waits on them (measured: the k = 256 steps of
   // config 2 run 25-35% faster; error ~2e-6).
   const char* chunk_env = std::getenv("QSG_TC_CHUNK");
-  if (chunk_env) p.chunk = std::max(1, chunk_blocks() / 2);
-  else p.chunk = p.kblocks <= 8 ? std::max(2, (p.kblocks + 1) / 2) : 2;
+  const int per128 = 128 / kb;  // k-blocks per 128 real K
+  if (chunk_env) p.chunk = std::max(1, chunk_blocks() * per128 / 4);
+  else p.chunk = p.kblocks <= 4 * per128 ? std::max(per128, (p.kblocks + 1) / 2) : per128;
   p.store_perm = g.store_perm ? 1 : 0;
   p.nrow_bits = g.nrow_bits;
   p.ncol_bits = g.ncol_bits;
@@ -1526,10 +1538,15 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                          Tc5Cfg<BN>::SMEM);
     cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Tc5Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN, 32>::SMEM);
     return resident_pairs(cgemm_f16_pair_kernel<BN, false>, Tc5Cfg<BN>::SMEM);
   }();
   const long long clusters = std::min<long long>(pairs, slots);
-  if (split)
+  if (split && kb == 32)
+    cgemm_f16_pair_kernel<BN, true, 32>
+        <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  else if (split)
     cgemm_f16_pair_kernel<BN, true>
         <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else
