@@ -27,8 +27,10 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     "1": {"circuit": (4, 4, 16, 0), "plan": "configs/config1_plan.json",
-          "workload": "config1: 4x4 RQC depth (1+16+1), greedy plan, 64-amplitude batch per x1 draw",
-          "slices_per_step": None},
+          "workload": "config1: 4x4 RQC depth (1+16+1), greedy plan, 64-amplitude batch per x1 draw; "
+                      "x1 batching: the plan widened to open the 10 x1 qubits serves all 1024 draws "
+                      "in one contraction (Engine.amplitude_batches)",
+          "slices_per_step": None, "x1_batch": 1024},
     "2": {"circuit": (7, 7, 32, 0), "plan": "configs/config2_plan.json",
           "workload": "config2: 7x7 RQC depth (1+32+1), reference 7x7 region order, 1 cut bond "
                       "b_007_003_004 (2 slices), 1024-amplitude batch per x1 draw",
@@ -133,11 +135,11 @@ def dist_setup():
 
 # ----------------------------------------------------------------------------- reference arm
 
-def cpu_reference_sample(cfg, steps_prefix: int, threads: int, seed: int = 0):
+def cpu_reference_sample(cfg, steps_prefix: int, threads: int, seed: int = 0, ntasks: int = 0):
     """Times the reference's own step kernels (oracle/_ref = unmodified qsim
     library, Eigen GEMM -> OpenBLAS 1-thread shim) over the first
-    `steps_prefix` plan steps of `threads` independent (x1, slice) tasks on
-    `threads` host threads.  Returns (seconds, flops)."""
+    `steps_prefix` plan steps of `ntasks` (default: `threads`) independent
+    (x1, slice) tasks on `threads` host threads.  Returns (seconds, flops)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import reflib
     import paper_1905_00444_b200 as Q
@@ -145,7 +147,14 @@ def cpu_reference_sample(cfg, steps_prefix: int, threads: int, seed: int = 0):
     text = Q.generate_rqc(r, c, m, s)
     plan = open(os.path.join(ROOT, cfg["plan"])).read()
     open_q = json.loads(plan)["open_qubits"]
-    return reflib.execute_prefix(text, plan, open_q, steps_prefix, threads, threads, seed)
+    return reflib.execute_prefix(text, plan, open_q, steps_prefix, ntasks or threads, threads, seed)
+
+
+def reference_tasks(plan_json: dict, nsteps: int, threads: int, budget_flops: float) -> int:
+    """Independent tasks per sample: one per thread, more for small plans so
+    the sample is ~budget_flops of CPU work (about 10-30 s)."""
+    prefix = sum(st["flops"] for st in plan_json["steps"][:nsteps]) or 1
+    return max(threads, min(1 << 20, int(budget_flops // prefix)))
 
 
 def reference_prefix_steps(plan_json: dict, budget_flops: float) -> int:
@@ -172,11 +181,12 @@ def run_reference_arm(args):
     batch = 1 << len(plan["open_qubits"])
     slices_per_batch = cfg.get("slices_per_batch") or plan["slices"]
     flops_per_step = plan["per_slice"]["flops"] * slices_per_batch
+    ntasks = reference_tasks(plan, nsteps, threads, args.cpu_budget_flops / 4)
     for _ in range(args.warmup):
-        cpu_reference_sample(cfg, nsteps, threads)
+        cpu_reference_sample(cfg, nsteps, threads, ntasks=threads)
     secs, flops = 0.0, 0
     for i in range(args.steps):
-        s, f = cpu_reference_sample(cfg, nsteps, threads, seed=i + 1)
+        s, f = cpu_reference_sample(cfg, nsteps, threads, seed=i + 1, ntasks=ntasks)
         secs += s
         flops += f
     rate = flops / secs  # Eq.(1) flop/s of the reference kernels on this host
@@ -192,7 +202,7 @@ def run_reference_arm(args):
                          "sample": f"reference qsim kernels (contract_ttgt + normalize_inplace, Eigen GEMM via "
                                    f"OpenBLAS 1-thread shim) over plan steps s000..s{nsteps - 1:03d} "
                                    f"({prefix_flops / plan['per_slice']['flops']:.2%} of a slice's Eq.1 flops) of "
-                                   f"{threads} independent (x1, slice) tasks per step on {threads} threads; "
+                                   f"{ntasks} independent (x1, slice) tasks per step on {threads} threads; "
                                    f"amplitudes/s extrapolated at the measured Eq.1 rate {rate / 1e9:.1f} Gflop/s"},
         "e2e": {"value": amps, "unit": "amplitudes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -220,11 +230,19 @@ def run_ours(args):
     plan = json.loads(plan_text)
     open_q = plan["open_qubits"]
     n = r * c
-    eng = Q.Engine(text, plan_text, device=local, tensor_cores=not args.no_tc, memory_budget=args.memory_budget)
+    xb = args.x1_batch if args.x1_batch is not None else cfg.get("x1_batch", 1)
+    closed = [q for q in range(n) if q not in open_q]
+    if xb > 1:
+        if cfg["slices_per_step"] is not None or len(closed) > 20 or xb > (1 << len(closed)):
+            raise SystemExit("--x1-batch needs batch mode, <= 20 x1 qubits and at most 2^#x1 draws")
+        eng_plan = Q.widen_plan(text, plan_text, closed)
+    else:
+        eng_plan = plan_text
+    eng = Q.Engine(text, eng_plan, device=local, tensor_cores=not args.no_tc, memory_budget=args.memory_budget)
     info = eng.info
     K = plan["slices"]
     per_step = cfg["slices_per_step"] or K
-    batch = info.batch_size
+    batch = xb * (1 << len(open_q))  # amplitudes delivered per run
 
     def slices_for(step_index: int):
         if cfg["slices_per_step"] is None:
@@ -233,7 +251,7 @@ def run_ours(args):
         return [(base + j) % K for j in range(per_step)]
 
     # ---- device-timed region: node tensors resident, slices back to back ----
-    x1 = Q.draw_x1(n, open_q, 0, rank)
+    x1 = Q.draw_x1(n, open_q, 0, rank) if xb == 1 else [-1] * n
     eng.prepare(x1)
     eng.synchronize()
     for w in range(args.warmup):
@@ -245,15 +263,32 @@ def run_ours(args):
         torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = eng.launches()
+    # Working sets below ~2x L2 (config 1): flush L2 (write 256 MiB) between
+    # steps, outside the per-step event windows.
+    small = info.arena_bytes < (256 << 20)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if small else None
     with ClockSampler(local) as clocks:
-        ev0.record(stream)
-        for i in range(args.steps):
-            eng.run(slices_for(args.warmup + i), reset=True, per_slice=True)
-        ev1.record(stream)
-        ev1.synchronize()
+        if small:
+            ms = 0.0
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            with torch.cuda.stream(stream):
+                for i in range(args.steps):
+                    flush.fill_(i & 255)
+                    evs[i][0].record(stream)
+                    eng.run(slices_for(args.warmup + i), reset=True, per_slice=True)
+                    evs[i][1].record(stream)
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+        else:
+            ev0.record(stream)
+            for i in range(args.steps):
+                eng.run(slices_for(args.warmup + i), reset=True, per_slice=True)
+            ev1.record(stream)
+            ev1.synchronize()
+            ms = ev0.elapsed_time(ev1)
     torch.cuda.synchronize()
     launches = eng.launches() - launches0
-    ms = ev0.elapsed_time(ev1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -279,13 +314,19 @@ def run_ours(args):
     # open-wire fold is resident since engine creation (uploaded once per
     # circuit, info.node_bytes), so no per-step H2D of node tensors exists.
     h2d = 0
-    d2h = batch * 16
+    d2h = info.batch_size * 16
+    # host inputs of every step (x1 draws, src/sampler.cpp:70-82) are made
+    # before the timed region; the API calls, kernels and D2H are inside it
+    host_x1 = [[Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)]
+               for i in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
     for i in range(args.steps):
-        x1i = Q.draw_x1(n, open_q, 1, rank * args.steps + i)
-        eng.amplitude_batch(x1i, slices_for(args.warmup + i))
+        if xb == 1:
+            eng.amplitude_batch(host_x1[i][0], slices_for(args.warmup + i))
+        else:
+            eng.amplitude_batches(open_q, host_x1[i], slices_for(args.warmup + i), bitstrings=False)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
@@ -352,8 +393,11 @@ def run_ours(args):
             "data": "synthetic (seeded RQC from generate_rqc, random x1 via mt19937_64)",
             "config": {"workload": cfg["workload"], "parallelism": (f"x1 batches across {world} GPU(s)" if cfg["slices_per_step"] is None else f"slices across {world} GPU(s)"),
                        "amplitudes_per_step_per_gpu": batch, "slices_per_step_per_gpu": per_step,
+                       **({"x1_draws_per_contraction": xb} if xb > 1 else {}),
                        "flops_per_step_per_gpu": info.flops_per_slice * per_step,
-                       "l2": "intermediates (up to 16 GiB) >> 126 MB L2; no flush needed",
+                       "l2": ("working set < 2x L2: 256 MiB L2 flush between steps, outside the per-step "
+                              "event windows" if small else
+                              f"working set ({info.arena_bytes / 2**30:.1f} GiB arena) >> 126 MB L2; no flush needed"),
                        "arena_bytes": info.arena_bytes, "tensor_cores": not args.no_tc,
                        **({"memory_budget": args.memory_budget} if args.memory_budget else {})},
             "tflops_eq1": tflops, "tflops_frac_fp32_simt": tflops / fp32_peak,
@@ -371,13 +415,16 @@ def run_ours(args):
         try:
             cpu_threads = args.cpu_threads or min(os.cpu_count() or 1, 32)
             nsteps = reference_prefix_steps(plan, args.cpu_budget_flops)
-            secs, fl = cpu_reference_sample(cfg, nsteps, cpu_threads)
+            ntasks = reference_tasks(plan, nsteps, cpu_threads, args.cpu_budget_flops / 4)
+            secs, fl = cpu_reference_sample(cfg, nsteps, cpu_threads, ntasks=ntasks)
             rate = fl / secs
-            cpu_amps = rate / (info.flops_per_slice * cfg.get("slices_per_batch", per_step)) * batch
+            # the reference runs the plan as given: its flops and batch per x1 draw
+            cpu_amps = (rate / (plan["per_slice"]["flops"] * cfg.get("slices_per_batch", per_step))
+                        * (1 << len(open_q)))
             line["cpu_baseline"] = {
                 "value": cpu_amps, "unit": "amplitudes/s", "cores": cpu_threads, "kind": "reference",
                 "sample": f"unmodified reference kernels (oracle/_ref, Eigen->OpenBLAS 1-thread shim) over plan "
-                          f"steps s000..s{nsteps - 1:03d} of {cpu_threads} (x1, slice) tasks on {cpu_threads} "
+                          f"steps s000..s{nsteps - 1:03d} of {ntasks} (x1, slice) tasks on {cpu_threads} "
                           f"threads in {secs:.1f} s; extrapolated at {rate / 1e9:.1f} Eq.1 Gflop/s"}
         except Exception as exc:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "amplitudes/s", "cores": 0, "kind": "reference",
@@ -401,6 +448,8 @@ def main():
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-out", default="", help="write the per-op profile (one JSON line per op) here")
+    ap.add_argument("--x1-batch", type=int, default=None,
+                    help="x1 draws per contraction via the widened plan (batch-mode configs; config 1 default 1024)")
     ap.add_argument("--memory-budget", type=int, default=0,
                     help="bytes per contraction (reference ExecOptions); larger steps run out of core")
     ap.add_argument("--cpu-threads", type=int, default=0)

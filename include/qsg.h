@@ -211,6 +211,19 @@ int qsg_engine_reset_profile(qsg_engine* e);
 int qsg_amplitude_batch(qsg_engine* e, const int* x1_bits, int n, const int64_t* slice_ids, int64_t k,
                         double* amps_host, char* bitstrings_host);
 
+/* GPU batching of many x1 draws (no reference counterpart; it serves
+ * amplitude_batch, src/sampler.cpp:111-120, for a list of draws).
+ * qsg_widen_plan: the plan (kind as qsg_plan_json) with extra qubits opened
+ * -- same order and cut -- as JSON; build the engine from it (kind 0).
+ * qsg_amplitude_batches: one contraction on that engine for nx1 draws (each
+ * n entries, -1 exactly on the nbase base open qubits; they may differ only
+ * on qubits the widened plan opened).  Writes nx1 x 2^nbase amplitudes
+ * (re, im) and bitstrings, each draw in the reference's batch order. */
+int qsg_widen_plan(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                   const int* extra_open, int nextra, char* buf, int64_t cap, int64_t* len);
+int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
+                          const int64_t* slice_ids, int64_t k, double* amps_host, char* bitstrings_host);
+
 /* run_amplitudes (src/engine.cpp:300-378) for closed plans: nb bitstrings
  * of n chars, fraction num/den (den <= 0: all slices), seed.  out: nb
  * complex128; ids_out (nullable): the k slice ids; flops: Eq.(1) total. */

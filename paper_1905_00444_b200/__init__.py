@@ -139,6 +139,8 @@ def lib():
         "qsg_engine_reset_profile": (i32, [vp]),
         "qsg_engine_set_profile": (i32, [vp, i32]),
         "qsg_amplitude_batch": (i32, [vp, P(i32), i32, P(i64), i64, dp, cp]),
+        "qsg_widen_plan": (i32, [cp, i32, cp, P(i32), i32, P(i32), i32, cp, i64, P(i64)]),
+        "qsg_amplitude_batches": (i32, [vp, P(i32), i32, P(i32), i32, i32, P(i64), i64, dp, cp]),
         "qsg_run_amplitudes": (i32, [vp, cp, i32, i32, i64, i64, u64, dp, P(i64), P(u64)]),
         "qsg_sample": (i32, [vp, i64, i64, i64, i32, C.c_double, u64, cp, dp, P(_SampleStats), P(_XebReport)]),
         "qsg_xeb_score": (i32, [i32, dp, i64, i32, C.c_double, P(_XebReport)]),
@@ -344,6 +346,15 @@ def program_listing(circuit_text: str, plan_text: str = "", kind: int = PLAN_JSO
                  0 if tensor_cores else 2, int(memory_budget))
 
 
+def widen_plan(circuit_text: str, plan_text: str, extra_open, kind: int = PLAN_JSON, open_qubits=()) -> str:
+    """The plan with extra qubits opened (same order and cut), as JSON -- an
+    engine built on it serves many x1 draws in one contraction
+    (Engine.amplitude_batches)."""
+    a, p = _i32(open_qubits)
+    e, pe = _i32(extra_open)
+    return _text(lib().qsg_widen_plan, circuit_text.encode(), kind, plan_text.encode(), p, len(a), pe, len(e))
+
+
 def xeb_score(n: int, probs, hog_median=None) -> dict:
     """xeb_score (src/sampler.cpp:187-215): cross entropy, 2^n<p>-1 fidelity, HOG fraction."""
     a = np.ascontiguousarray(np.asarray(probs, dtype=np.float64))
@@ -478,6 +489,26 @@ class Engine:
         raw = bits.raw
         n = len(a)
         return [raw[i * n:(i + 1) * n].decode() for i in range(self.info.batch_size)], amps.view(np.complex128)
+
+    def amplitude_batches(self, base_open, x1_list, slice_ids, bitstrings: bool = True):
+        """amplitude_batch for many x1 draws in ONE contraction on an engine built
+        from widen_plan(...): per draw (bitstrings, complex128 amplitudes), or with
+        bitstrings=False the [draws, 2^|open|] amplitude array alone."""
+        b, pb = _i32(base_open)
+        xs = np.ascontiguousarray(np.asarray(x1_list, dtype=np.int32))
+        nx1, n = xs.shape
+        ids = np.ascontiguousarray(np.asarray(list(slice_ids), dtype=np.int64))
+        per = 1 << len(b)
+        amps = np.zeros(2 * per * nx1, dtype=np.float64)
+        bits = C.create_string_buffer(max(1, n * per * nx1)) if bitstrings else None
+        _check(lib().qsg_amplitude_batches(self._h, pb, len(b), _p(xs, C.c_int), nx1, n, _p(ids, C.c_int64), len(ids),
+                                           _p(amps, C.c_double), bits))
+        amps = amps.view(np.complex128).reshape(nx1, per)
+        if not bitstrings:
+            return amps
+        raw = bits.raw
+        return [([raw[(t * per + j) * n:(t * per + j + 1) * n].decode() for j in range(per)], amps[t])
+                for t in range(nx1)]
 
     def sample(self, num_samples: int, fraction=(0, 0), amplitude_fraction: bool = False, cap: float = 6.0,
                seed: int = 0):

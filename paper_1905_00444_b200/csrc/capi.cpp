@@ -589,6 +589,36 @@ int qsg_amplitude_batch(qsg_engine* e, const int* x1_bits, int n, const int64_t*
   });
 }
 
+int qsg_widen_plan(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                   const int* extra_open, int nextra, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    const qsg::Circuit c = qsg::parse_circuit(circuit_text);
+    const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
+    put_text(qsg::plan_to_json(qsg::widen_plan(c, plan, std::vector<int>(extra_open, extra_open + nextra))), buf, cap,
+             len);
+  });
+}
+
+int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
+                          const int64_t* slice_ids, int64_t k, double* amps_host, char* bitstrings_host) {
+  return guarded([&] {
+    std::vector<std::vector<int>> xs;
+    for (int t = 0; t < nx1; ++t)
+      xs.emplace_back(x1_list + static_cast<std::size_t>(t) * n, x1_list + static_cast<std::size_t>(t + 1) * n);
+    const auto res = qsg::amplitude_batches(*e->impl, std::vector<int>(base_open, base_open + nbase), xs,
+                                            std::vector<std::int64_t>(slice_ids, slice_ids + k),
+                                            bitstrings_host != nullptr);
+    std::size_t o = 0;
+    for (const auto& draw : res)
+      for (const auto& [bits, amp] : draw) {
+        amps_host[2 * o] = amp.real();
+        amps_host[2 * o + 1] = amp.imag();
+        if (bitstrings_host) std::memcpy(bitstrings_host + o * static_cast<std::size_t>(n), bits.data(), static_cast<std::size_t>(n));
+        ++o;
+      }
+  });
+}
+
 int qsg_run_amplitudes(qsg_engine* e, const char* bitstrings, int nb, int n, int64_t frac_num, int64_t frac_den,
                        uint64_t seed, double* out, int64_t* ids_out, uint64_t* flops) {
   return guarded([&] {

@@ -839,6 +839,84 @@ std::vector<std::pair<std::string, cdouble>> amplitude_batch(Engine& e, const st
   return out;
 }
 
+ContractionPlan widen_plan(const Circuit& c, const ContractionPlan& plan, const std::vector<int>& extra_open) {
+  std::set<int> open(plan.open_qubits.begin(), plan.open_qubits.end());
+  for (int q : extra_open) {
+    if (q < 0 || q >= c.num_qubits()) throw std::invalid_argument("widen_plan: qubit out of range");
+    open.insert(q);
+  }
+  ContractionPlan p = plan;
+  p.open_qubits.assign(open.begin(), open.end());
+  annotate_plan(fold_shape(c, p.open_qubits), p);  // same order and cut, wider open wires
+  return p;
+}
+
+std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
+    Engine& wide, const std::vector<int>& base_open, const std::vector<std::vector<int>>& x1_list,
+    const std::vector<std::int64_t>& slice_ids, bool with_bitstrings) {
+  const int n = wide.circuit().num_qubits();
+  const auto& wopen = wide.plan().open_qubits;
+  std::vector<char> is_open(static_cast<std::size_t>(n), 0), is_base(static_cast<std::size_t>(n), 0);
+  for (int q : wopen) is_open[static_cast<std::size_t>(q)] = 1;
+  if (!std::is_sorted(base_open.begin(), base_open.end()))
+    throw std::invalid_argument("amplitude_batches: base open qubits must be sorted (the plan's order)");
+  for (int q : base_open) {
+    if (q < 0 || q >= n || !is_open[static_cast<std::size_t>(q)])
+      throw std::invalid_argument("amplitude_batches: base open qubits must be open in the widened plan");
+    is_base[static_cast<std::size_t>(q)] = 1;
+  }
+  if (x1_list.empty()) return {};
+  // One contraction: the widened plan's closed qubits must agree across the list.
+  std::vector<int> x1w(static_cast<std::size_t>(n), -1);
+  for (int q = 0; q < n; ++q) {
+    if (is_open[static_cast<std::size_t>(q)]) continue;
+    x1w[static_cast<std::size_t>(q)] = x1_list[0][static_cast<std::size_t>(q)];
+  }
+  for (const auto& x1 : x1_list) {
+    if (static_cast<int>(x1.size()) != n) throw std::invalid_argument("fold: bitstring length != qubit count");
+    for (int q = 0; q < n; ++q) {
+      const int b = x1[static_cast<std::size_t>(q)];
+      if ((b < 0) != static_cast<bool>(is_base[static_cast<std::size_t>(q)]))
+        throw std::invalid_argument("x1 open qubits do not match the plan's open qubits");
+      if (b > 1) throw std::invalid_argument("fold: output bits must be 0, 1 or -1 (open)");
+      if (!is_open[static_cast<std::size_t>(q)] && b != x1w[static_cast<std::size_t>(q)])
+        throw std::invalid_argument("amplitude_batches: x1 draws differ on a qubit the widened plan keeps closed");
+    }
+  }
+  wide.prepare(x1w);
+  wide.run(slice_ids, /*reset=*/true, /*per_slice=*/false);
+  std::vector<cdouble> amps;
+  wide.results(&amps, nullptr);
+  // Batch index of a full bitstring: bit (|open|-1-r) <-> r-th smallest open qubit (src/sampler.cpp:41-52).
+  const std::size_t nw = wopen.size(), nb = base_open.size();
+  std::vector<std::vector<std::pair<std::string, cdouble>>> out(x1_list.size());
+  for (std::size_t t = 0; t < x1_list.size(); ++t) {
+    auto& dst = out[t];
+    dst.reserve(std::size_t{1} << nb);
+    // wide index = fixed part (this draw's bits on the extra open qubits) +
+    // the base batch index's bits scattered to the base qubits' positions
+    std::size_t fixed = 0;
+    std::vector<std::size_t> base_pos(nb);
+    for (std::size_t r = 0; r < nw; ++r) {
+      const int q = wopen[r];
+      const std::size_t bit = std::size_t{1} << (nw - 1 - r);
+      const auto it = std::find(base_open.begin(), base_open.end(), q);
+      if (it == base_open.end()) {
+        if (x1_list[t][static_cast<std::size_t>(q)] == 1) fixed |= bit;
+      } else {
+        base_pos[static_cast<std::size_t>(it - base_open.begin())] = bit;  // base r-th smallest <-> batch bit nb-1-r
+      }
+    }
+    for (std::size_t j = 0; j < (std::size_t{1} << nb); ++j) {
+      std::size_t idx = fixed;
+      for (std::size_t r = 0; r < nb; ++r)
+        if ((j >> (nb - 1 - r)) & 1) idx |= base_pos[r];
+      dst.emplace_back(with_bitstrings ? merge_bits(x1_list[t], base_open, j) : std::string(), amps[idx]);
+    }
+  }
+  return out;
+}
+
 AmplitudeOutput run_amplitudes(Engine& e, const std::vector<std::string>& bitstrings, Fraction f, std::uint64_t seed) {
   const int n = e.circuit().num_qubits();
   if (!e.plan().open_qubits.empty()) throw std::invalid_argument("run_amplitudes: plan must close every output");

@@ -202,4 +202,15 @@ struct AmplitudeOutput {
 // run_amplitudes (src/engine.cpp:300-378) for closed plans.
 AmplitudeOutput run_amplitudes(Engine& e, const std::vector<std::string>& bitstrings, Fraction f, std::uint64_t seed);
 
+// Many x1 draws in one contraction (GPU batching of amplitude_batch): the
+// plan with the x1 qubits that vary across draws opened as well -- same
+// order and cut, every draw's 2^|open| amplitudes are entries of the wider
+// batch.  widen_plan annotates it; amplitude_batches runs an engine built
+// on it once and gathers each draw's (bitstring, amplitude) list in the
+// reference's order (src/sampler.cpp:111-120).
+ContractionPlan widen_plan(const Circuit& c, const ContractionPlan& plan, const std::vector<int>& extra_open);
+std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
+    Engine& wide, const std::vector<int>& base_open, const std::vector<std::vector<int>>& x1_list,
+    const std::vector<std::int64_t>& slice_ids, bool with_bitstrings = true);
+
 }  // namespace qsg

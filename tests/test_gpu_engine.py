@@ -297,3 +297,30 @@ def test_out_of_core_indivisible(gpu):
     text, plan, _ = _small_config2_like(gpu, depth=12)
     with pytest.raises(gpu.QsgError, match="indivisible contraction still over budget"):
         gpu.Engine(text, plan, memory_budget=64)
+
+
+def test_amplitude_batches_widened_plan(gpu):
+    """Many x1 draws in one contraction: config 1's plan with every x1 qubit
+    opened (same order / cut) serves 64 draws x 64 amplitudes at once;
+    each draw's list equals the per-draw amplitude_batch (bit-exact
+    bitstrings, amplitudes to FP32 level) and the oracle."""
+    import qsim_oracle as O
+    text = gpu.generate_rqc(4, 4, 16, 0)
+    plan = open(os.path.join(ROOT, "configs", "config1_plan.json")).read()
+    base = json.loads(plan)["open_qubits"]
+    closed = [q for q in range(16) if q not in base]
+    wide = gpu.widen_plan(text, plan, closed)
+    draws = [gpu.draw_x1(16, base, 0, i) for i in range(64)]
+    with gpu.Engine(text, wide) as e:
+        got = e.amplitude_batches(base, draws, [0])
+    with gpu.Engine(text, plan) as e:
+        for x1, (bits, amps) in zip(draws[:8], got[:8]):
+            rbits, ramps = e.amplitude_batch(x1, [0])
+            assert bits == rbits
+            assert rel(amps, ramps) < 1e-5
+    for x1, (bits, amps) in zip(draws[:4], got[:4]):
+        obits, oamps = O.amplitude_batch(text, plan, x1, [0])
+        assert bits == obits and rel(amps, oamps) < 1e-5
+    with pytest.raises(gpu.InvalidArgument, match="closed"):
+        with gpu.Engine(text, gpu.widen_plan(text, plan, closed[:2])) as e:
+            e.amplitude_batches(base, draws, [0])
