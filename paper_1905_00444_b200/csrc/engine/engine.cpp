@@ -107,7 +107,8 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
     check(cudaMalloc(&ooc_scratch_, static_cast<std::size_t>(ooc_slot_bytes_) * static_cast<std::size_t>(depth)),
           "out-of-core scratch cudaMalloc");
     check(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
-    ooc_ev_.resize(2 * static_cast<std::size_t>(depth) + 2);
+    check(cudaStreamCreateWithFlags(&store_stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ooc_ev_.resize(3 * static_cast<std::size_t>(depth) + 2);
     for (auto& e : ooc_ev_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   }
   check(cudaMalloc(&metas_, sizeof(dev::TMeta) * static_cast<std::size_t>(std::max(nmeta_, 1))), "meta cudaMalloc");
@@ -146,6 +147,7 @@ Engine::~Engine() {
   if (ooc_scratch_) cudaFree(ooc_scratch_);
   for (auto e : ooc_ev_) cudaEventDestroy(e);
   if (copy_stream_) cudaStreamDestroy(copy_stream_);
+  if (store_stream_) cudaStreamDestroy(store_stream_);
   if (metas_) cudaFree(metas_);
   if (acc_) cudaFree(acc_);
   if (per_slice_) cudaFree(per_slice_);
@@ -350,16 +352,40 @@ void Engine::compile() {
                      (step_working_set(8 * xm * k, 8 * k * yn, 8 * xm * yn) > opt_.memory_budget ||
                       bufs_[static_cast<std::size_t>(X.buf)].host || bufs_[static_cast<std::size_t>(Y.buf)].host);
     View A = X, B = Y;
+    // An out-of-core step gathers its operands' blocks per piece instead
+    // (no permuted host copy): the view is just reordered.
+    auto reorder = [](const View& v, const std::vector<Label>& order) {
+      View r = v;
+      r.labels = order;
+      r.dims.clear();
+      r.strides.clear();
+      for (const auto& l : order) {
+        r.dims.push_back(v.dim_of(l));
+        r.strides.push_back(v.stride_of(l));
+      }
+      return r;
+    };
+    bool a_gather = false, b_gather = false;
     if (!best.use_a) {
       std::vector<Label> order = xfree;
       order.insert(order.end(), best.con.begin(), best.con.end());
-      A = permute_to(X, order, static_cast<int>(si), ooc);
+      if (ooc) {
+        A = reorder(X, order);
+        a_gather = true;
+      } else {
+        A = permute_to(X, order, static_cast<int>(si), ooc);
+      }
       best.ta = false;
     }
     if (!best.use_b) {
       std::vector<Label> order = best.con;
       order.insert(order.end(), yfree.begin(), yfree.end());
-      B = permute_to(Y, order, static_cast<int>(si), ooc);
+      if (ooc) {
+        B = reorder(Y, order);
+        b_gather = true;
+      } else {
+        B = permute_to(Y, order, static_cast<int>(si), ooc);
+      }
       best.tb = false;
     }
     // Free-label orders as laid out in the operands.
@@ -390,6 +416,18 @@ void Engine::compile() {
     touch(B.buf);
     g.c = new_buf(g.m * g.n * 8);
     g.ooc = ooc;
+    g.a_gather = a_gather;
+    g.b_gather = b_gather;
+    if (a_gather) {
+      g.ga_ext = A.dims;
+      g.ga_str = A.strides;
+      g.ga_split = xfree.size();
+    }
+    if (b_gather) {
+      g.gb_ext = B.dims;
+      g.gb_str = B.strides;
+      g.gb_split = best.con.size();
+    }
     if (ooc) {
       bufs_[static_cast<std::size_t>(g.c)].host = true;
       g.tc = opt_.tensor_cores;  // decided per piece
@@ -539,6 +577,35 @@ std::vector<std::array<std::int64_t, 4>> Engine::decompose_pieces(std::int64_t m
   return out;
 }
 
+// K1 gather of one piece block on the copy stream: dims [lo, hi) of the
+// (ext, str) view carry the split index; the block [r0, r0 + rp) fixes their
+// leading digits (rp divides their product, r0 % rp == 0), the other dims
+// stay whole.  Output dense in the view's order.
+void Engine::gather_block(const char* src, std::vector<std::int64_t> ext, const std::vector<std::int64_t>& str,
+                          std::size_t lo, std::size_t hi, std::int64_t r0, std::int64_t rp, char* dst, int* launches) {
+  std::int64_t base = 0, place = 1;
+  for (std::size_t i = hi; i-- > lo;) {
+    const std::int64_t e = ext[i], digit = (r0 / place) % e;
+    if (place * e > rp) {
+      base += digit * str[i];
+      ext[i] = place < rp ? rp / place : 1;  // straddling dim keeps a sub-range, higher ones a single digit
+    }
+    place *= e;
+  }
+  std::vector<std::int64_t> e2, s2;
+  for (std::size_t i = 0; i < ext.size(); ++i)
+    if (ext[i] > 1) {
+      e2.push_back(ext[i]);
+      s2.push_back(str[i]);
+    }
+  if (e2.empty()) {
+    e2.push_back(1);
+    s2.push_back(1);
+  }
+  check(dev::permute(src, base, dst, static_cast<int>(e2.size()), e2.data(), s2.data(), copy_stream_, launches),
+        "ooc gather");
+}
+
 // Five-stage pipeline of one out-of-core GEMM (src/engine.cpp:52-180):
 // acquire a scratch slot, load the A row block and B column block
 // (host->device copies on the copy stream; 2-D copies for strided blocks),
@@ -551,9 +618,13 @@ void Engine::launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node
   const char* B = static_cast<const char*>(ptr(op.b, node_off));
   char* C = base_of(op.c);
   const std::int64_t k = op.k;
-  cudaEvent_t start = ooc_ev_[2 * static_cast<std::size_t>(depth)], done = ooc_ev_[2 * static_cast<std::size_t>(depth) + 1];
+  // Loads (H2D) on copy_stream_, stores (D2H) on store_stream_: both link
+  // directions stay busy; per-slot events order the reuse of a slot.
+  const std::size_t nd = static_cast<std::size_t>(depth);
+  cudaEvent_t start = ooc_ev_[3 * nd], done = ooc_ev_[3 * nd + 1];
   check(cudaEventRecord(start, stream_), "event");
   check(cudaStreamWaitEvent(copy_stream_, start, 0), "wait");
+  check(cudaStreamWaitEvent(store_stream_, start, 0), "wait");
   for (std::size_t i = 0; i < op.pieces.size(); ++i) {
     const auto& pc = op.pieces[i];
     const std::int64_t m0 = pc[0], mp = pc[1], n0 = pc[2], np = pc[3];
@@ -562,9 +633,12 @@ void Engine::launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node
     char* sB = sA + align_up(mp * k * 8);
     char* sC = sB + align_up(k * np * 8);
     char* sW = sC + align_up(mp * np * 8);
-    cudaEvent_t loaded = ooc_ev_[2 * slot], computed = ooc_ev_[2 * slot + 1];
-    // load (copy stream, in order after the previous store of this slot)
-    if (!op.ta)
+    cudaEvent_t loaded = ooc_ev_[3 * slot], computed = ooc_ev_[3 * slot + 1], stored = ooc_ev_[3 * slot + 2];
+    // load: after the slot's previous GEMM has read its A / B blocks
+    if (i >= nd) check(cudaStreamWaitEvent(copy_stream_, computed, 0), "wait");
+    if (op.a_gather) {
+      gather_block(A, op.ga_ext, op.ga_str, 0, op.ga_split, m0, mp, sA, launches);
+    } else if (!op.ta)
       check(cudaMemcpyAsync(sA, A + m0 * k * 8, static_cast<std::size_t>(mp * k * 8), cudaMemcpyDefault, copy_stream_),
             "ooc load A");
     else
@@ -572,7 +646,9 @@ void Engine::launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node
                               static_cast<std::size_t>(mp * 8), static_cast<std::size_t>(k), cudaMemcpyDefault,
                               copy_stream_),
             "ooc load A");
-    if (op.tb)
+    if (op.b_gather)
+      gather_block(B, op.gb_ext, op.gb_str, op.gb_split, op.gb_ext.size(), n0, np, sB, launches);
+    else if (op.tb)
       check(cudaMemcpyAsync(sB, B + n0 * k * 8, static_cast<std::size_t>(np * k * 8), cudaMemcpyDefault, copy_stream_),
             "ooc load B");
     else
@@ -581,8 +657,9 @@ void Engine::launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node
                               copy_stream_),
             "ooc load B");
     check(cudaEventRecord(loaded, copy_stream_), "event");
-    // execute (engine stream)
+    // execute (engine stream): after the load, and after the slot's previous C block was stored
     check(cudaStreamWaitEvent(stream_, loaded, 0), "wait");
+    if (i >= nd) check(cudaStreamWaitEvent(stream_, stored, 0), "wait");
     dev::GemmArgs g{};
     g.a = sA;
     g.b = sB;
@@ -603,14 +680,15 @@ void Engine::launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node
     if (tc) check(dev::cgemm_tc(g, stream_, launches), "cgemm_tc");
     else check(dev::cgemm(g, stream_, launches), "cgemm");
     check(cudaEventRecord(computed, stream_), "event");
-    // store (copy stream)
-    check(cudaStreamWaitEvent(copy_stream_, computed, 0), "wait");
+    // store (store stream)
+    check(cudaStreamWaitEvent(store_stream_, computed, 0), "wait");
     check(cudaMemcpy2DAsync(C + (m0 * op.n + n0) * 8, static_cast<std::size_t>(op.n * 8), sC,
                             static_cast<std::size_t>(np * 8), static_cast<std::size_t>(np * 8),
-                            static_cast<std::size_t>(mp), cudaMemcpyDefault, copy_stream_),
+                            static_cast<std::size_t>(mp), cudaMemcpyDefault, store_stream_),
           "ooc store C");
+    check(cudaEventRecord(stored, store_stream_), "event");
   }
-  check(cudaEventRecord(done, copy_stream_), "event");
+  check(cudaEventRecord(done, store_stream_), "event");
   check(cudaStreamWaitEvent(stream_, done, 0), "wait");
 }
 

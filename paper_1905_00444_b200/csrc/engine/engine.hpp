@@ -135,6 +135,13 @@ class Engine {
     // through the device pipeline; C in host memory.
     bool ooc = false;
     std::vector<std::array<std::int64_t, 4>> pieces;
+    // Out-of-core operand gathers: instead of a K1 permute into a host copy,
+    // each piece's block is gathered (K1) straight from the source view
+    // (extents / strides in GEMM order; A: split rows = first ga_split
+    // dims, B: split columns = dims from gb_split on).
+    bool a_gather = false, b_gather = false;
+    std::vector<std::int64_t> ga_ext, ga_str, gb_ext, gb_str;
+    std::size_t ga_split = 0, gb_split = 0;
   };
 
   void compile();
@@ -146,6 +153,8 @@ class Engine {
                                                                    std::int64_t budget);
   void launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot);
   void launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node_off, int* launches);
+  void gather_block(const char* src, std::vector<std::int64_t> ext, const std::vector<std::int64_t>& str,
+                    std::size_t lo, std::size_t hi, std::int64_t r0, std::int64_t rp, char* dst, int* launches);
 
   Circuit circuit_;
   ContractionPlan plan_;
@@ -173,7 +182,8 @@ class Engine {
   char* host_arena_ = nullptr;
   std::int64_t ooc_slot_bytes_ = 0;
   char* ooc_scratch_ = nullptr;
-  cudaStream_t copy_stream_ = nullptr;
+  cudaStream_t copy_stream_ = nullptr;   // out-of-core loads (H2D)
+  cudaStream_t store_stream_ = nullptr;  // out-of-core stores (D2H)
   std::vector<cudaEvent_t> ooc_ev_;
   dev::TMeta* metas_ = nullptr;
   int nmeta_ = 0;
