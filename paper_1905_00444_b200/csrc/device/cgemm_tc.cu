@@ -100,6 +100,7 @@ struct TcParams {
   int c_split;         // fp16 kernel: write C split
   int log2k;           // ceil(log2(k)): the split output's bound exponent
   long long c_total;   // complex elements of C (offset of the lo plane / 4 bytes)
+  int stream_store;    // fp16 kernel: evict-first (st.global.cs) output stores
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
@@ -1184,12 +1185,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (p.c_split) {
                 const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
                 const float2 g0 = __half22float2(h0), g1 = __half22float2(h1);
-                *reinterpret_cast<uint2*>(c_bytes + 4 * o) = make_uint2(h2_bits(h0), h2_bits(h1));
-                *reinterpret_cast<uint2*>(c_bytes + lo_plane + 4 * o) =
-                    make_uint2(h2_bits(__floats2half2_rn(v.x - g0.x, v.y - g0.y)),
-                               h2_bits(__floats2half2_rn(v.z - g1.x, v.w - g1.y)));
+                if (p.stream_store) {
+                  __stcs(reinterpret_cast<uint2*>(c_bytes + 4 * o), make_uint2(h2_bits(h0), h2_bits(h1)));
+                  __stcs(reinterpret_cast<uint2*>(c_bytes + lo_plane + 4 * o),
+                         make_uint2(h2_bits(__floats2half2_rn(v.x - g0.x, v.y - g0.y)),
+                                    h2_bits(__floats2half2_rn(v.z - g1.x, v.w - g1.y))));
+                } else {
+                  *reinterpret_cast<uint2*>(c_bytes + 4 * o) = make_uint2(h2_bits(h0), h2_bits(h1));
+                  *reinterpret_cast<uint2*>(c_bytes + lo_plane + 4 * o) =
+                      make_uint2(h2_bits(__floats2half2_rn(v.x - g0.x, v.y - g0.y)),
+                                 h2_bits(__floats2half2_rn(v.z - g1.x, v.w - g1.y)));
+                }
               } else {
-                *reinterpret_cast<float4*>(p.c + 2 * o) = v;
+                if (p.stream_store) __stcs(reinterpret_cast<float4*>(p.c + 2 * o), v);
+                else *reinterpret_cast<float4*>(p.c + 2 * o) = v;
               }
             }
             __syncwarp();
@@ -1511,6 +1520,7 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   while ((std::int64_t{1} << l2k) < g.k) ++l2k;
   p.log2k = l2k;
   p.c_total = g.m * g.n;
+  p.stream_store = std::getenv("QSG_TC_STCS") && std::getenv("QSG_TC_STCS")[0] == '0' ? 0 : 1;  // measured ~2% on config 2
   p.meta_a = meta_a;
   p.meta_b = meta_b;
   p.meta_c = g.meta_c;
