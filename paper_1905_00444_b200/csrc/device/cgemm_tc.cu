@@ -1498,9 +1498,10 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                             const __half* blo, unsigned int* sync, const __half* ahi, const __half* alo,
                             cudaStream_t stream) {
   const bool split = ahi != nullptr;
-  // Pre-split A: pure TMA -> MMA stages; 32-K stages (6 in flight instead
-  // of 3) hide more HBM latency where A streams from DRAM (QSG_TC_KB).
-  const int kb = split && (2 * g.k) % 32 == 0 ? (env_int("QSG_TC_KB", 64) == 32 ? 32 : 64) : BK16;
+  // 64-K stages (3 in flight).  32-K stages (6 in flight, SW64 planes; the
+  // kernel's kBK = 32 instantiation) measured 2-6% slower: the per-stage
+  // barrier / commit overhead outweighs the deeper TMA lookahead.
+  const int kb = BK16;
   const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM, kb) : make_map(g.a, 2 * g.k, g.m, BM);
   const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM, kb) : ma;
   const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
@@ -1548,15 +1549,10 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                          Tc5Cfg<BN>::SMEM);
     cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Tc5Cfg<BN>::SMEM);
-    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Tc5Cfg<BN, 32>::SMEM);
     return resident_pairs(cgemm_f16_pair_kernel<BN, false>, Tc5Cfg<BN>::SMEM);
   }();
   const long long clusters = std::min<long long>(pairs, slots);
-  if (split && kb == 32)
-    cgemm_f16_pair_kernel<BN, true, 32>
-        <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
-  else if (split)
+  if (split)
     cgemm_f16_pair_kernel<BN, true>
         <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else

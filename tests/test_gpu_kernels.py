@@ -141,7 +141,7 @@ def test_cgemm_device_shapes_vs_fp64(gpu, m, n, k, ta, tb):
                                       (1 << 14, 16, 256, 0), (2048, 32, 64, 1), (1024, 64, 512, 0), (768, 48, 32, 0),
                                       # fp16 kernel with a half k-block tail (2k % 64 == 32)
                                       (512, 128, 16, 0), (1024, 64, 48, 1), (256, 32, 80, 0)])
-@pytest.mark.parametrize("prec", ["f16", "f16split", "f16split32", "tf32"])
+@pytest.mark.parametrize("prec", ["f16", "f16split", "tf32"])
 def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb, prec, monkeypatch):
     """tcgen05 path (3xFP16 with operand scaling on CTA-pair shapes, 3xTF32
     otherwise or with QSG_TC_PREC=tf32): FP32-level accuracy (1e-5 relative
@@ -149,7 +149,6 @@ def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb, prec, monkeypatch):
     import torch
     monkeypatch.setenv("QSG_TC_PREC", "tf32" if prec == "tf32" else "f16")
     monkeypatch.setenv("QSG_TC_SPLITA", "1" if prec.startswith("f16split") else "0")
-    monkeypatch.setenv("QSG_TC_KB", "32" if prec == "f16split32" else "64")
     g = torch.Generator().manual_seed(m + 3 * n + 7 * k)
     A = torch.complex(torch.rand(m, k, generator=g) - 0.5, torch.rand(m, k, generator=g) - 0.5)
     B = torch.complex(torch.rand(k, n, generator=g) - 0.5, torch.rand(k, n, generator=g) - 0.5)
