@@ -909,6 +909,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      bool sync_wait = true;
       for (long long ti = 0; ti < my_tiles; ++ti) {
         long long m_pair;
         int n_tile;
@@ -928,7 +929,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (p.sync && gk % p.sync_every == 0) {
             const long long c = gk / p.sync_every;
             atomicAdd(p.sync + c, 1u);
-            if (c >= 1) {
+            if (c >= 1 && sync_wait) {
               // pairs whose run reaches k-block (c-1)*every: all with base
               // tiles if it falls inside those, else the `extra` ones.
               const long long kprev = (c - 1) * p.sync_every;
@@ -936,12 +937,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const long long have = kprev < base * kblocks ? min(nclusters, total)
                                      : (kprev < (base + 1) * kblocks ? extra : 0);
               const unsigned need = 2u * static_cast<unsigned>(have);
-              for (int spin = 0; spin < 4096; ++spin) {  // bounded: never a deadlock, at worst unsynchronised
+              // Bounded spin: never a deadlock.  A wait that times out means
+              // some pairs are not co-resident (other work on the GPU); this
+              // producer then stops waiting for the rest of the launch.
+              int spin = 0;
+              for (; spin < 4096; ++spin) {
                 unsigned v;
                 asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.sync + c - 1) : "memory");
                 if (v >= need) break;
                 __nanosleep(128);
               }
+              if (spin == 4096) sync_wait = false;
             }
           }
           mbar_wait(&empty[s], ph ^ 1);
