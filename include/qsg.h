@@ -61,6 +61,15 @@ int qsg_flop_count(uint64_t v0, uint64_t v1, uint64_t v2, uint64_t* flops);
 int qsg_generate_rqc(int rows, int cols, int m, uint64_t seed, int t_only_first, char* buf, int64_t cap,
                      int64_t* len);
 
+/* generate_rqc on a masked grid (no reference counterpart; its generator is
+ * rectangle-only, src/circuit.cpp:227-241): mask = rows*cols '0'/'1' chars;
+ * CZ layouts keep only active-active edges, inactive cells get only the
+ * cycle-0 and final H.  qsg_bristlecone_mask: the 11x12 diamond with 72,
+ * 70 or 60 active cells (SURVEY 8d construction). */
+int qsg_generate_rqc_masked(int rows, int cols, const char* mask, int m, uint64_t seed, int t_only_first, char* buf,
+                            int64_t cap, int64_t* len);
+int qsg_bristlecone_mask(int active, char* buf, int64_t cap, int64_t* len);
+
 /* serialize_circuit(parse_circuit(text)); src/circuit.cpp:128-220 */
 int qsg_canonical_circuit(const char* text, char* buf, int64_t cap, int64_t* len);
 

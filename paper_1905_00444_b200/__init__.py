@@ -108,6 +108,8 @@ def lib():
         "qsg_flop_count": (i32, [u64, u64, u64, P(u64)]),
         "qsg_generate_rqc": (i32, [i32, i32, i32, u64, i32, cp, i64, P(i64)]),
         "qsg_canonical_circuit": (i32, [cp, cp, i64, P(i64)]),
+        "qsg_generate_rqc_masked": (i32, [i32, i32, cp, i32, u64, i32, cp, i64, P(i64)]),
+        "qsg_bristlecone_mask": (i32, [i32, cp, i64, P(i64)]),
         "qsg_circuit_info": (i32, [cp, P(i32), P(i32), P(i32), P(i32)]),
         "qsg_plan_json": (i32, [cp, P(i32), i32, i32, cp, i64, cp, i64, P(i64)]),
         "qsg_fold_qtns": (i32, [cp, P(i32), i32, cp, i64, cp, i64, P(i64)]),
@@ -218,6 +220,16 @@ def flop_count(v0: int, v1: int, v2: int) -> int:
 def generate_rqc(rows: int, cols: int, m: int, seed: int, t_only_first: bool = True) -> str:
     """serialize_circuit(generate_rqc(...)) (src/circuit.cpp:243-294)."""
     return _text(lib().qsg_generate_rqc, rows, cols, m, seed, 1 if t_only_first else 0)
+
+
+def generate_rqc_masked(rows: int, cols: int, mask: str, m: int, seed: int, t_only_first: bool = True) -> str:
+    """generate_rqc on a masked grid (mask: rows*cols '0'/'1'); inactive cells only get the outer H layers."""
+    return _text(lib().qsg_generate_rqc_masked, rows, cols, mask.encode(), m, seed, 1 if t_only_first else 0)
+
+
+def bristlecone_mask(active: int = 70) -> str:
+    """11x12 diamond mask with 72, 70 or 60 active cells (the Bristlecone construction of SURVEY 8d)."""
+    return _text(lib().qsg_bristlecone_mask, active)
 
 
 def canonical_circuit(text: str) -> str:

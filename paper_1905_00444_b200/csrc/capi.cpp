@@ -175,6 +175,18 @@ int qsg_generate_rqc(int rows, int cols, int m, uint64_t seed, int t_only_first,
   });
 }
 
+int qsg_generate_rqc_masked(int rows, int cols, const char* mask, int m, uint64_t seed, int t_only_first, char* buf,
+                            int64_t cap, int64_t* len) {
+  return guarded([&] {
+    put_text(qsg::serialize_circuit(qsg::generate_rqc_masked(rows, cols, mask ? mask : "", m, seed, t_only_first != 0)),
+             buf, cap, len);
+  });
+}
+
+int qsg_bristlecone_mask(int active, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] { put_text(qsg::bristlecone_mask(active), buf, cap, len); });
+}
+
 int qsg_canonical_circuit(const char* text, char* buf, int64_t cap, int64_t* len) {
   return guarded([&] { put_text(qsg::serialize_circuit(qsg::parse_circuit(text)), buf, cap, len); });
 }

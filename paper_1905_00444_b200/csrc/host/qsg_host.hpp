@@ -71,6 +71,9 @@ struct CircuitError : std::runtime_error {
 Circuit parse_circuit(const std::string& text, int rows_hint = 0, int cols_hint = 0);
 std::string serialize_circuit(const Circuit& c);
 Circuit generate_rqc(int rows, int cols, int m, std::uint64_t seed, bool t_only_first = true);
+Circuit generate_rqc_masked(int rows, int cols, const std::string& mask, int m, std::uint64_t seed,
+                            bool t_only_first = true);
+std::string bristlecone_mask(int active);  // 11x12 diamond: 72, 70 or 60 active cells
 int cz_layout_of_cycle(int c);
 std::vector<std::pair<int, int>> cz_layout_edges(int layout, int rows, int cols);
 void validate_circuit(const Circuit& c);

@@ -324,3 +324,23 @@ def test_amplitude_batches_widened_plan(gpu):
     with pytest.raises(gpu.InvalidArgument, match="closed"):
         with gpu.Engine(text, gpu.widen_plan(text, plan, closed[:2])) as e:
             e.amplitude_batches(base, draws, [0])
+
+
+def test_masked_grid_amplitudes_vs_state_vector(gpu):
+    """A masked 4x5 grid (3 idle cells, depth 1+12+1) through the greedy plan:
+    amplitudes match the double state vector; an idle cell's output 1 has
+    amplitude 0 (its worldline is H.H = I)."""
+    import qsim_oracle as O
+    mask = "11111" "10111" "11101" "01111"
+    text = gpu.generate_rqc_masked(4, 5, mask, 12, 7)
+    opn = [0, 5, 6, 7, 12]  # qubit 6 is an idle cell (mask row 1 = 10111)
+    plan = gpu.plan_json(text, opn, gpu.PLAN_GREEDY)
+    sv = O.evolve(text)
+    x1 = [-1 if q in opn else (q * 7 + 3) % 2 for q in range(20)]
+    x1 = [b if mask[q] == "1" or b < 0 else 0 for q, b in enumerate(x1)]  # idle closed cells read 0
+    with gpu.Engine(text, plan) as e:
+        bits, amps = e.amplitude_batch(x1, [0])
+    exact = np.array([sv[int(b, 2)] for b in bits])
+    assert rel(amps, exact) < 1e-4
+    idle_one = np.array([b[6] == "1" for b in bits])
+    assert np.all(np.abs(amps[idle_one]) < 1e-7 * np.abs(amps).max())

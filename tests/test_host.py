@@ -158,3 +158,26 @@ def test_flop_count():
     assert Q.flop_count(2**30, 2**30, 2**30) == 8 << 45
     with pytest.raises(Q.InvalidArgument):
         Q.flop_count(2, 3, 5)
+
+
+def test_masked_generator_and_bristlecone_masks():
+    """masked-grid RQCs.  All-ones mask = generate_rqc
+    (bit-exact text); inactive cells carry only the two H layers; CZs only
+    join active neighbours; the Bristlecone diamond masks have 72/70/60 cells."""
+    assert Q.generate_rqc_masked(5, 5, "1" * 25, 20, 3) == Q.generate_rqc(5, 5, 20, 3)
+    counts = {a: Q.bristlecone_mask(a).count("1") for a in (72, 70, 60)}
+    assert counts == {72: 72, 70: 70, 60: 60}
+    mask = Q.bristlecone_mask(70)
+    text = Q.generate_rqc_masked(11, 12, mask, 32, 0)
+    lines = [l.split() for l in text.splitlines()[2:]]
+    for f in lines:
+        qs = [int(x) for x in f[2:]]
+        if f[1] != "h":
+            assert all(mask[q] == "1" for q in qs), f
+        if f[1] == "cz":
+            a, b = qs
+            assert abs(a - b) in (1, 12)
+    inactive = [q for q in range(132) if mask[q] == "0"]
+    assert all(sum(1 for f in lines if int(f[2]) == q) == 2 for q in inactive[:10])
+    with pytest.raises(Q.InvalidArgument):
+        Q.generate_rqc_masked(3, 3, "101", 8, 0)
