@@ -94,7 +94,7 @@ struct TcParams {
   int norm_a, norm_b;
   int chunk;   // k-blocks per TMEM promotion chunk
   int group_m;    // m-pairs per rasterization group (fp16 kernel)
-  unsigned int* sync;  // fp16 kernel: per-(wave, checkpoint) arrival counters (null: no K-sync)
+  unsigned int* sync;  // fp16 kernel: K-sync arrival counters per checkpoint of the persistent run (null: off)
   int sync_every;      // k-blocks between checkpoints
   int a_presplit;      // fp16 kernel: A stored split (TMeta::split_exp), see GemmArgs
   int c_split;         // fp16 kernel: write C split
@@ -1327,16 +1327,8 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-CUtensorMapL2promotion l2_promo() {
-  const char* env = std::getenv("QSG_TC_L2PROMO");
-  if (!env) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  switch (std::atoi(env)) {
-    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
-    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
-    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  }
-}
+// TMA L2 promotion 256 B (measured best of none / 64 / 128 / 256 B on s026).
+constexpr CUtensorMapL2promotion kL2Promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
 
 // 2-D fp32 K-major map: inner dim `cols` (contiguous), outer `rows`; box
 // [box_rows x 32] with 128-byte swizzle.
@@ -1347,17 +1339,15 @@ CUtensorMap make_map(const void* base, long long cols, long long rows, int box_r
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(BK), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promo(),
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, kL2Promo,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
 }
 
-// Row pitch (elements) of the fp16 B_r^T planes: 2k plus QSG_TC_BPAD (experiment).
-long long b16_pitch(std::int64_t k) {
-  const char* env = std::getenv("QSG_TC_BPAD");
-  return 2 * k + (env ? std::atoll(env) : 0);
-}
+// Row pitch (elements) of the fp16 B_r^T planes (padding the pitch was
+// measured: no gain, more DRAM traffic).
+long long b16_pitch(std::int64_t k) { return 2 * k; }
 
 // fp16 map: inner dim `cols` (contiguous), box [box_rows x kb] with kb = 64
 // (128 B rows, SW128) or 32 (64 B rows, SW64).
@@ -1370,7 +1360,7 @@ CUtensorMap make_map_f16(const void* base, long long cols, long long rows, long 
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, l2_promo(),
+                                 kb == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, kL2Promo,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
