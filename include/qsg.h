@@ -159,7 +159,9 @@ int qsg_engine_create(const char* circuit_text, int kind, const char* plan_text,
  * run through a pipeline of pipeline_depth pieces in flight
  * (src/engine.cpp:52-180); its tensors live in pinned host memory and only
  * the pieces occupy the device.  Error "indivisible contraction still over
- * budget" (runtime error) as the reference. */
+ * budget" (runtime error) as the reference.  memory_budget -1: automatic --
+ * everything in HBM if the program fits the device's free memory, else the
+ * largest power-of-two budget whose out-of-core program fits. */
 int qsg_engine_create_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
                          int device, int flags, int64_t memory_budget, int pipeline_depth, qsg_engine** out);
 int qsg_engine_destroy(qsg_engine* e);
@@ -169,9 +171,11 @@ int qsg_engine_destroy(qsg_engine* e);
  * and CPU-side checks.  Arguments as qsg_engine_create. */
 int qsg_program_listing(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
                         int flags, char* buf, int64_t cap, int64_t* len);
-/* As qsg_program_listing with a memory budget (out-of-core placement). */
+/* As qsg_program_listing with a memory budget (out-of-core placement);
+ * memory_budget -1 = automatic for a device of device_memory bytes. */
 int qsg_program_listing_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
-                           int flags, int64_t memory_budget, char* buf, int64_t cap, int64_t* len);
+                           int flags, int64_t memory_budget, int64_t device_memory, char* buf, int64_t cap,
+                           int64_t* len);
 
 typedef struct qsg_engine_info {
   int64_t num_qubits, num_slices, batch_size, num_steps, max_rank;

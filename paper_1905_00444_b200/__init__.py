@@ -124,7 +124,7 @@ def lib():
         "qsg_normalize": (i32, [fp, i64, dp, P(i32)]),
         "qsg_engine_create": (i32, [cp, i32, cp, P(i32), i32, i32, i32, P(vp)]),
         "qsg_engine_create_ex": (i32, [cp, i32, cp, P(i32), i32, i32, i32, i64, i32, P(vp)]),
-        "qsg_program_listing_ex": (i32, [cp, i32, cp, P(i32), i32, i32, i64, cp, i64, P(i64)]),
+        "qsg_program_listing_ex": (i32, [cp, i32, cp, P(i32), i32, i32, i64, i64, cp, i64, P(i64)]),
         "qsg_engine_destroy": (i32, [vp]),
         "qsg_program_listing": (i32, [cp, i32, cp, P(i32), i32, i32, cp, i64, P(i64)]),
         "qsg_engine_get_info": (i32, [vp, P(_EngineInfo)]),
@@ -350,12 +350,13 @@ def normalize_inplace(data: np.ndarray, log_scale: float = 0.0):
 
 
 def program_listing(circuit_text: str, plan_text: str = "", kind: int = PLAN_JSON, open_qubits=(),
-                    tensor_cores: bool = True, memory_budget: int = 0) -> str:
+                    tensor_cores: bool = True, memory_budget: int = 0, device_memory: int = 0) -> str:
     """Device program the engine would run (no GPU needed): ops, GEMM shapes/paths, arena bytes;
-    with memory_budget > 0 the out-of-core placement (host arena, piece counts)."""
+    with memory_budget > 0 the out-of-core placement (host arena, piece counts); memory_budget=-1
+    picks it automatically for a device of device_memory bytes (default 180 GB)."""
     a, p = _i32(open_qubits)
     return _text(lib().qsg_program_listing_ex, circuit_text.encode(), kind, plan_text.encode(), p, len(a),
-                 0 if tensor_cores else 2, int(memory_budget))
+                 0 if tensor_cores else 2, int(memory_budget), int(device_memory))
 
 
 def widen_plan(circuit_text: str, plan_text: str, extra_open, kind: int = PLAN_JSON, open_qubits=()) -> str:

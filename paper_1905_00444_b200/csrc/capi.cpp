@@ -460,7 +460,8 @@ int qsg_engine_create_ex(const char* circuit_text, int kind, const char* plan_te
                          int device, int flags, int64_t memory_budget, int pipeline_depth, qsg_engine** out) {
   return guarded([&] {
     require_device();
-    if (memory_budget < 0 || pipeline_depth < 1) throw std::invalid_argument("engine: memory_budget >= 0, pipeline_depth >= 1");
+    if (memory_budget < -1 || pipeline_depth < 1)
+      throw std::invalid_argument("engine: memory_budget >= -1 (-1: automatic), pipeline_depth >= 1");
     const qsg::Circuit c = qsg::parse_circuit(circuit_text);
     const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
     qsg::EngineOptions o;
@@ -476,7 +477,8 @@ int qsg_engine_create_ex(const char* circuit_text, int kind, const char* plan_te
 }
 
 int qsg_program_listing_ex(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
-                           int flags, int64_t memory_budget, char* buf, int64_t cap, int64_t* len) {
+                           int flags, int64_t memory_budget, int64_t device_memory, char* buf, int64_t cap,
+                           int64_t* len) {
   return guarded([&] {
     const qsg::Circuit c = qsg::parse_circuit(circuit_text);
     const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
@@ -484,6 +486,7 @@ int qsg_program_listing_ex(const char* circuit_text, int kind, const char* plan_
     o.compile_only = true;
     o.tensor_cores = (flags & QSG_ENGINE_NO_TENSOR_CORES) == 0;
     o.memory_budget = memory_budget;
+    o.device_memory = device_memory;
     qsg::Engine e(c, plan, o);
     put_text(e.describe(), buf, cap, len);
   });

@@ -92,9 +92,36 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
   for (int q : plan_.open_qubits) closed_[static_cast<std::size_t>(q)] = 0;
   node_x1_off_.assign(static_cast<std::size_t>(nq), 0);
   batch_ = std::int64_t{1} << plan_.open_qubits.size();
-  compile();
-  split_handoffs();
-  pack_buffers();
+  auto build = [&] {
+    ooc_slot_bytes_ = 0;
+    compile();
+    split_handoffs();
+    pack_buffers();
+  };
+  if (opt_.memory_budget >= 0) {
+    build();
+  } else {
+    // Automatic: the in-HBM program if it fits the device, else the largest
+    // power-of-two contraction budget whose out-of-core program fits.
+    std::int64_t avail = opt_.device_memory;
+    if (avail <= 0 && !opt_.compile_only) {
+      std::size_t free_b = 0, total_b = 0;
+      check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      avail = static_cast<std::int64_t>(free_b);
+    }
+    if (avail <= 0) avail = std::int64_t{180} << 30;
+    avail = avail / 100 * 92;  // headroom for the CUDA context, metas, accumulators
+    auto device_need = [&] {
+      return arena_bytes_ + ooc_slot_bytes_ * std::max(1, opt_.pipeline_depth);
+    };
+    opt_.memory_budget = 0;
+    build();
+    for (std::int64_t b = std::int64_t{1} << 42; device_need() > avail; b >>= 1) {
+      if (b < (std::int64_t{1} << 20)) throw std::runtime_error("engine: no contraction budget fits the device memory");
+      opt_.memory_budget = b;
+      build();
+    }
+  }
   op_ms_.assign(ops_.size(), 0.0);
   op_execs_.assign(ops_.size(), 0);
   if (opt_.compile_only) return;  // program listing only (no device)

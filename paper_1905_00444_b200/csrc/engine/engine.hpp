@@ -45,8 +45,11 @@ struct EngineOptions {
   // bytes runs as pieces (src/plan.cpp:355-472) through a device-side
   // pipeline of depth pipeline_depth (src/engine.cpp:52-180); its operands
   // and result live in pinned host memory.  0 = everything in HBM.
+  // < 0: automatic -- in HBM if the program fits device_memory (0: the
+  // device's free memory), else the largest power-of-two budget that fits.
   std::int64_t memory_budget = 0;
   int pipeline_depth = 2;
+  std::int64_t device_memory = 0;
 };
 
 struct OpProfile {
@@ -71,6 +74,7 @@ class Engine {
   const ContractionPlan& plan() const { return plan_; }
   std::int64_t batch_size() const { return batch_; }
   std::int64_t arena_bytes() const { return arena_bytes_; }
+  std::int64_t memory_budget() const { return opt_.memory_budget; }  // the resolved budget (0 = all in HBM)
   std::int64_t host_arena_bytes() const { return host_arena_bytes_; }
   std::int64_t node_bytes() const { return node_bytes_; }
   cudaStream_t stream() const { return stream_; }

@@ -54,3 +54,16 @@ def test_out_of_core_placement():
     assert sum(int(f[10]) for f in (l.split() for l in lines) if f[0] == "gemm") == json.loads(plan)["per_slice"]["flops"]
     with pytest.raises(Q.QsgError, match="indivisible"):
         Q.program_listing(text, plan, memory_budget=4096)
+
+
+def test_out_of_core_automatic_budget():
+    """memory_budget=-1: in HBM when the program fits the device, else the
+    largest power-of-two contraction budget whose out-of-core program fits."""
+    text = Q.generate_rqc(7, 7, 32, 0)
+    plan = open(os.path.join(ROOT, "configs", "config2_plan.json")).read()
+    big = Q.program_listing(text, plan, memory_budget=-1, device_memory=180 << 30).splitlines()
+    assert "host arena" not in big[0] and not any(" ooc " in l for l in big)
+    for dev in (30 << 30, 12 << 30):
+        head = Q.program_listing(text, plan, memory_budget=-1, device_memory=dev).splitlines()[0].split()
+        arena, slot = int(head[1]), int(head[head.index("scratch") + 1])
+        assert arena + 2 * slot <= 0.92 * dev
