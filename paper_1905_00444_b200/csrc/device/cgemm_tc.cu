@@ -1177,6 +1177,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               for (int b = 3; b < 7; ++b)
                 if (b < p.ncol_bits && ((jhi >> b) & 1)) jc_off += 1ll << p.col_pos[b];
             }
+            if (p.c_split) {
+              // Split output, 4 complex per lane: one 16-byte hi and one
+              // 16-byte lo store (half the store instructions of 2 complex).
+              long long jc = 0;  // column bits 3..6 of this 8-complex run
+              if (p.store_perm) {
+                const int jhi = c0 >> 1;
+#pragma unroll
+                for (int b = 3; b < 7; ++b)
+                  if (b < p.ncol_bits && ((jhi >> b) & 1)) jc += 1ll << p.col_pos[b];
+              }
+#pragma unroll
+              for (int it = 0; it < 2; ++it) {
+                const int r = it * 16 + (lane >> 1), hf = lane & 1;
+                const float4 v0 = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 8 * hf);
+                const float4 v1 = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 8 * hf + 4);
+                long long o;  // complex offset of v0.xy (col bits 0..2 are the output's bits 0..2)
+                if (p.store_perm) {
+                  const long long ro = __shfl_sync(0xffffffffu, my_row_off, r);
+                  o = ro + col_tile_off + jc + 4 * hf;
+                } else {
+                  o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 8 * hf) >> 1;
+                }
+                const float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                uint32_t hh[4], ll[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const __half2 h = __floats2half2_rn(x[2 * j], x[2 * j + 1]);
+                  const float2 g = __half22float2(h);
+                  hh[j] = h2_bits(h);
+                  ll[j] = h2_bits(__floats2half2_rn(x[2 * j] - g.x, x[2 * j + 1] - g.y));
+                }
+                if (p.stream_store) {
+                  __stcs(reinterpret_cast<uint4*>(c_bytes + 4 * o), make_uint4(hh[0], hh[1], hh[2], hh[3]));
+                  __stcs(reinterpret_cast<uint4*>(c_bytes + lo_plane + 4 * o), make_uint4(ll[0], ll[1], ll[2], ll[3]));
+                } else {
+                  *reinterpret_cast<uint4*>(c_bytes + 4 * o) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+                  *reinterpret_cast<uint4*>(c_bytes + lo_plane + 4 * o) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+                }
+              }
+              __syncwarp();
+              continue;
+            }
 #pragma unroll
             for (int it = 0; it < 4; ++it) {
               const int r = it * 8 + (lane >> 2), c4 = lane & 3;
@@ -1188,24 +1230,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               } else {
                 o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) >> 1;
               }
-              if (p.c_split) {
-                const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
-                const float2 g0 = __half22float2(h0), g1 = __half22float2(h1);
-                if (p.stream_store) {
-                  __stcs(reinterpret_cast<uint2*>(c_bytes + 4 * o), make_uint2(h2_bits(h0), h2_bits(h1)));
-                  __stcs(reinterpret_cast<uint2*>(c_bytes + lo_plane + 4 * o),
-                         make_uint2(h2_bits(__floats2half2_rn(v.x - g0.x, v.y - g0.y)),
-                                    h2_bits(__floats2half2_rn(v.z - g1.x, v.w - g1.y))));
-                } else {
-                  *reinterpret_cast<uint2*>(c_bytes + 4 * o) = make_uint2(h2_bits(h0), h2_bits(h1));
-                  *reinterpret_cast<uint2*>(c_bytes + lo_plane + 4 * o) =
-                      make_uint2(h2_bits(__floats2half2_rn(v.x - g0.x, v.y - g0.y)),
-                                 h2_bits(__floats2half2_rn(v.z - g1.x, v.w - g1.y)));
-                }
-              } else {
-                if (p.stream_store) __stcs(reinterpret_cast<float4*>(p.c + 2 * o), v);
-                else *reinterpret_cast<float4*>(p.c + 2 * o) = v;
-              }
+              if (p.stream_store) __stcs(reinterpret_cast<float4*>(p.c + 2 * o), v);
+              else *reinterpret_cast<float4*>(p.c + 2 * o) = v;
             }
             __syncwarp();
           }
