@@ -112,12 +112,21 @@ int qsg_permute_dev(const void* in_dev, int64_t base, void* out_dev, int rank, c
 int qsg_cgemm_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_a,
                   int trans_b, void* stream);
 
-/* K2 on the tcgen05 tensor cores (3xTF32, FP32-level accuracy).  Requires
- * m % 128 == 0, n % 64 == 0, k % 16 == 0, A row-major; returns
- * QSG_ERR_INVALID_ARGUMENT otherwise.  Allocates its B-expansion workspace
- * (32*n*k bytes) internally and synchronises the stream. */
+/* K2 on the tcgen05 tensor cores at FP32-level accuracy: CTA-pair 3xFP16
+ * with power-of-two operand scaling when m % 256 == 0 (the production
+ * path), 3xTF32 otherwise (QSG_TC_PREC=tf32 forces it).  Requires
+ * m % 128 == 0, 2n % 32 == 0, k % 16 == 0, A row-major; returns
+ * QSG_ERR_INVALID_ARGUMENT otherwise.  Allocates its workspace (operand
+ * maxima, B / A plane expansion) internally and synchronises the stream. */
 int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_b,
                      void* stream);
+
+/* K3: acc[i] += double(fin[i]) * 2^log_scale for i < count (complex128
+ * acc), and per_slice[i] = that contribution when per_slice_dev is not NULL.
+ * The per-slice accumulation of batch_amplitudes (src/sampler.cpp:28-34).
+ * Synchronises the stream. */
+int qsg_accumulate_dev(const void* fin_dev, double log_scale, int64_t count, void* acc_dev, void* per_slice_dev,
+                       void* stream);
 
 /* ---------------------------------------------------------------------------
  * Tensor operations on host buffers, computed on the GPU (synchronous)

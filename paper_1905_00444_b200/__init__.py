@@ -118,6 +118,7 @@ def lib():
         "qsg_permute_dev": (i32, [vp, i64, vp, i32, P(i64), P(i64), vp]),
         "qsg_cgemm_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, vp]),
         "qsg_cgemm_tc_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, vp]),
+        "qsg_accumulate_dev": (i32, [vp, C.c_double, i64, vp, vp, vp]),
         "qsg_transpose": (i32, [i32, P(i64), fp, P(i32), fp]),
         "qsg_contract": (i32, [i32, P(i32), P(i64), fp, C.c_double, i32, P(i32), P(i64), fp, C.c_double, i32, P(i32),
                                fp, dp, P(u64), i32]),

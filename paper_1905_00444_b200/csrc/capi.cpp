@@ -288,6 +288,21 @@ int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t 
   });
 }
 
+int qsg_accumulate_dev(const void* fin_dev, double log_scale, int64_t count, void* acc_dev, void* per_slice_dev,
+                       void* stream) {
+  return guarded([&] {
+    if (count < 0) throw std::invalid_argument("accumulate: negative count");
+    DevBuf meta(sizeof(qsg::dev::TMeta));
+    qsg::dev::TMeta h{};
+    h.log_scale = log_scale;
+    auto s = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaMemcpyAsync(meta.p, &h, sizeof h, cudaMemcpyHostToDevice, s), "H2D");
+    cuda_check(qsg::dev::accumulate(fin_dev, meta.as<qsg::dev::TMeta>(), count, acc_dev, per_slice_dev, s),
+               "accumulate");
+    cuda_check(cudaStreamSynchronize(s), "accumulate sync");
+  });
+}
+
 int qsg_transpose(int rank, const int64_t* dims, const float* in_host, const int* perm, float* out_host) {
   return guarded([&] {
     std::vector<std::int64_t> d(dims, dims + rank);

@@ -192,3 +192,17 @@ def test_cgemm_tensor_core_dynamic_range(gpu, prec, monkeypatch):
     assert float(row_err[near].max()) < 1e-5
     abs_err = float((got - want).abs().max() / want.abs().max())
     assert abs_err < 5e-6
+
+
+def test_accumulate_kernel_matches_fp64(gpu):
+    """K3 (batch_amplitudes accumulation, src/sampler.cpp:28-34) through the C
+    ABI: acc += double(fin) * 2^log_scale, per-slice contribution kept."""
+    import torch
+    g = torch.Generator().manual_seed(5)
+    fin = torch.complex(torch.rand(1024, generator=g), torch.rand(1024, generator=g)).cuda()
+    acc = torch.ones(1024, dtype=torch.complex128, device="cuda")
+    per = torch.zeros(1024, dtype=torch.complex128, device="cuda")
+    gpu._check(gpu.lib().qsg_accumulate_dev(fin.data_ptr(), -3.0, 1024, acc.data_ptr(), per.data_ptr(), None))
+    want = fin.cpu().to(torch.complex128) * 2.0 ** -3
+    assert torch.equal(per.cpu(), want)
+    assert torch.equal(acc.cpu(), want + 1)
