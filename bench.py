@@ -389,7 +389,7 @@ def run_ours(args):
         line = {
             "metric": "amplitudes_per_sec", "value": value, "unit": "amplitudes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (fp32 accumulate)",
+            "scaling": "weak", "vs_baseline": None, "dtype": ("c64 (tensor cores: 3xFP16 split of fp32 operands, fp32 accumulate)" if not args.no_tc else "c64 (fp32 FFMA)"),
             "data": "synthetic (seeded RQC from generate_rqc, random x1 via mt19937_64)",
             "config": {"workload": cfg["workload"], "parallelism": (f"x1 batches across {world} GPU(s)" if cfg["slices_per_step"] is None else f"slices across {world} GPU(s)"),
                        "amplitudes_per_step_per_gpu": batch, "slices_per_step_per_gpu": per_step,
