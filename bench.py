@@ -157,6 +157,73 @@ def reference_tasks(plan_json: dict, nsteps: int, threads: int, budget_flops: fl
     return max(threads, min(1 << 20, int(budget_flops // prefix)))
 
 
+def step_mnk(st: dict):
+    """(m, n, k) of a plan step from its annotation: flops = 8 sqrt(vl vr vo),
+    intensity = flops / (8 (vl + vr + vo)), volume = vo."""
+    import math
+    f8 = st["flops"] / 8.0
+    vo = float(st["volume"])
+    s = st["flops"] / (8.0 * st["intensity"]) - vo  # vl + vr
+    p = f8 * f8 / vo                                # vl * vr
+    d = math.sqrt(max(s * s - 4 * p, 0.0))
+    vl, vr = (s + d) / 2, (s - d) / 2
+    k = math.sqrt(vl * vr / vo)
+    return int(round(vl / k)), int(round(vr / k)), int(round(k))
+
+
+def cpu_heavy_gemm_rate(plan_json: dict, threads: int, reps: int = 4):
+    """Eq.(1) rate of the reference's contract_ttgt + normalize_inplace on the
+    heavy step class (steps >= 1% of a slice's flops), measured on a
+    scaled-down copy of the largest step (m, k cut to <= 1024 / 4096; n <=
+    4096) run concurrently on `threads` host threads.  Returns (rate, desc)."""
+    import threading as th
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import reflib
+    top = max(plan_json["steps"], key=lambda x: x["flops"])
+    m, n, k = step_mnk(top)
+    m, n, k = min(m, 1024), min(n, 4096), min(k, 4096)
+    rng = np.random.default_rng(0)
+    a = (rng.random((m, k)) + 1j * rng.random((m, k))).astype(np.complex64)
+    b = (rng.random((k, n)) + 1j * rng.random((k, n))).astype(np.complex64)
+    out = {"flops": 0}
+    lock = th.Lock()
+
+    def work():
+        for _ in range(reps):
+            _, _, fl = reflib.contract_step([0, 1], a, 0.0, [1, 2], b, 0.0, [0, 2], True)
+            with lock:
+                out["flops"] += fl
+    ts = [th.Thread(target=work) for _ in range(threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    secs = time.perf_counter() - t0
+    rate = out["flops"] / secs
+    return rate, (f"heavy steps at {rate / 1e9:.1f} Eq.1 Gflop/s, measured on a {m}x{n}x{k} contract_ttgt "
+                  f"(scaled-down s{plan_json['steps'].index(top):03d}) x{threads} threads in {secs:.1f} s")
+
+
+def heavy_unmeasured(plan_json: dict, nsteps: int) -> float:
+    """Flops of the heavy steps (>= 1% of a slice) outside the measured prefix."""
+    total = plan_json["per_slice"]["flops"]
+    return sum(st["flops"] for st in plan_json["steps"][nsteps:] if st["flops"] >= 0.01 * total)
+
+
+def cpu_composite_amps(plan_json: dict, cfg, prefix_rate: float, heavy_rate: float, per_step: int,
+                       nsteps: int) -> float:
+    """Amplitudes/s of the reference on this host: heavy steps beyond the
+    measured prefix at the heavy GEMM rate, everything else at the measured
+    plan-prefix rate."""
+    total = plan_json["per_slice"]["flops"]
+    heavy = heavy_unmeasured(plan_json, nsteps)
+    secs_per_slice = heavy / heavy_rate + (total - heavy) / prefix_rate
+    slices = cfg.get("slices_per_batch") or per_step
+    return (1 << len(plan_json["open_qubits"])) / (secs_per_slice * slices)
+
+
 def reference_prefix_steps(plan_json: dict, budget_flops: float) -> int:
     """Longest plan prefix whose Eq.(1) flops stay within budget_flops (>= 1 step)."""
     acc, n = 0, 0
@@ -189,21 +256,25 @@ def run_reference_arm(args):
         s, f = cpu_reference_sample(cfg, nsteps, threads, seed=i + 1, ntasks=ntasks)
         secs += s
         flops += f
-    rate = flops / secs  # Eq.(1) flop/s of the reference kernels on this host
-    amps = rate / flops_per_step * batch
+    rate = flops / secs  # Eq.(1) flop/s of the reference kernels on this host (plan prefix)
+    heavy_rate, heavy_desc = (cpu_heavy_gemm_rate(plan, threads) if heavy_unmeasured(plan, nsteps) > 0
+                              else (rate, "no heavy steps beyond the prefix"))
+    amps = cpu_composite_amps(plan, cfg, rate, heavy_rate, slices_per_batch, nsteps)
+    rate_eff = amps / batch * flops_per_step
     line = {
         "metric": "amplitudes_per_sec", "value": amps, "unit": "amplitudes/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c64 (fp32)",
         "data": "synthetic (seeded RQC, random x1)",
         "config": {"workload": cfg["workload"], "parallelism": f"{threads} host threads"},
-        "tflops_eq1": rate / 1e12,
+        "tflops_eq1": rate_eff / 1e12,
         "cpu_baseline": {"value": amps, "unit": "amplitudes/s", "cores": threads, "kind": "reference",
                          "sample": f"reference qsim kernels (contract_ttgt + normalize_inplace, Eigen GEMM via "
                                    f"OpenBLAS 1-thread shim) over plan steps s000..s{nsteps - 1:03d} "
                                    f"({prefix_flops / plan['per_slice']['flops']:.2%} of a slice's Eq.1 flops) of "
-                                   f"{ntasks} independent (x1, slice) tasks per step on {threads} threads; "
-                                   f"amplitudes/s extrapolated at the measured Eq.1 rate {rate / 1e9:.1f} Gflop/s"},
+                                   f"{ntasks} independent (x1, slice) tasks per step on {threads} threads at "
+                                   f"{rate / 1e9:.1f} Eq.1 Gflop/s; {heavy_desc}; amplitudes/s = batch / "
+                                   f"(heavy flops / heavy rate + other flops / prefix rate)"},
         "e2e": {"value": amps, "unit": "amplitudes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -418,14 +489,16 @@ def run_ours(args):
             ntasks = reference_tasks(plan, nsteps, cpu_threads, args.cpu_budget_flops / 4)
             secs, fl = cpu_reference_sample(cfg, nsteps, cpu_threads, ntasks=ntasks)
             rate = fl / secs
+            heavy_rate, heavy_desc = (cpu_heavy_gemm_rate(plan, cpu_threads) if heavy_unmeasured(plan, nsteps) > 0
+                                      else (rate, "no heavy steps beyond the prefix"))
             # the reference runs the plan as given: its flops and batch per x1 draw
-            cpu_amps = (rate / (plan["per_slice"]["flops"] * cfg.get("slices_per_batch", per_step))
-                        * (1 << len(open_q)))
+            cpu_amps = cpu_composite_amps(plan, cfg, rate, heavy_rate, per_step, nsteps)
             line["cpu_baseline"] = {
                 "value": cpu_amps, "unit": "amplitudes/s", "cores": cpu_threads, "kind": "reference",
                 "sample": f"unmodified reference kernels (oracle/_ref, Eigen->OpenBLAS 1-thread shim) over plan "
                           f"steps s000..s{nsteps - 1:03d} of {ntasks} (x1, slice) tasks on {cpu_threads} "
-                          f"threads in {secs:.1f} s; extrapolated at {rate / 1e9:.1f} Eq.1 Gflop/s"}
+                          f"threads in {secs:.1f} s at {rate / 1e9:.1f} Eq.1 Gflop/s; {heavy_desc}; "
+                          f"amplitudes/s = batch / (heavy flops / heavy rate + other flops / prefix rate)"}
         except Exception as exc:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "amplitudes/s", "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {exc}"}
