@@ -201,6 +201,18 @@ int qsg_engine_open_qubits(qsg_engine* e, int* out /* num_open entries */);
 
 /* Fold for x1 (n entries, -1 exactly on the open qubits) and upload. */
 int qsg_engine_prepare(qsg_engine* e, const int* x1_bits, int n, int64_t* h2d_bytes);
+/* Node region (the open fold: info.node_bytes of complex64, engine order).
+ * A new instance of the same circuit layout (same grid, depth and CZ
+ * pattern; e.g. another single-qubit gate draw) reuses the engine's plan,
+ * arena and kernels: fold it on the host (qsg_engine_fold_nodes; fails if the
+ * fold shape differs), then qsg_engine_load_nodes (async H2D on the engine
+ * stream; pass pinned memory to overlap, keep it alive until the next
+ * synchronize).  This is the reference's per-circuit tensor construction,
+ * fold_worldlines at src/network.cpp:106-155, with the upload split out.
+ * qsg_engine_export_nodes copies the resident region back (synchronises). */
+int qsg_engine_fold_nodes(qsg_engine* e, const char* circuit_text, void* host_nodes, int64_t bytes);
+int qsg_engine_load_nodes(qsg_engine* e, const void* host_nodes, int64_t bytes);
+int qsg_engine_export_nodes(qsg_engine* e, void* host_nodes, int64_t bytes);
 /* Run slices (async, engine stream).  reset: zero the batch accumulator;
  * per_slice: keep each slice's contribution. */
 int qsg_engine_run(qsg_engine* e, const int64_t* slice_ids, int64_t k, int reset, int per_slice);

@@ -133,6 +133,9 @@ def lib():
         "qsg_engine_describe": (i32, [vp, cp, i64, P(i64)]),
         "qsg_engine_open_qubits": (i32, [vp, P(i32)]),
         "qsg_engine_prepare": (i32, [vp, P(i32), i32, P(i64)]),
+        "qsg_engine_fold_nodes": (i32, [vp, cp, vp, i64]),
+        "qsg_engine_load_nodes": (i32, [vp, vp, i64]),
+        "qsg_engine_export_nodes": (i32, [vp, vp, i64]),
         "qsg_engine_run": (i32, [vp, P(i64), i64, i32, i32]),
         "qsg_engine_results": (i32, [vp, dp, dp]),
         "qsg_engine_stream": (i32, [vp, P(vp)]),
@@ -380,6 +383,19 @@ def xeb_score(n: int, probs, hog_median=None) -> dict:
 
 # ---- engine ---------------------------------------------------------------
 
+def _buffer(buf):
+    """(pointer, bytes) of a contiguous numpy array or host torch tensor."""
+    if isinstance(buf, np.ndarray):
+        if not buf.flags["C_CONTIGUOUS"]:
+            raise ValueError("buffer must be contiguous")
+        return buf.ctypes.data, buf.nbytes
+    if hasattr(buf, "data_ptr"):
+        if buf.is_cuda or not buf.is_contiguous():
+            raise ValueError("buffer must be a contiguous host tensor")
+        return buf.data_ptr(), buf.numel() * buf.element_size()
+    raise TypeError("buffer must be a numpy array or a torch tensor")
+
+
 @dataclass
 class EngineInfo:
     num_qubits: int
@@ -449,6 +465,31 @@ class Engine:
         b = C.c_int64(0)
         _check(lib().qsg_engine_prepare(self._h, p, len(a), C.byref(b)))
         return b.value
+
+    def fold_nodes(self, circuit_text: str, out=None):
+        """Host open fold of another instance of this circuit layout, packed
+        as the engine's node region (complex64, node_bytes); `out` may be a
+        caller buffer (numpy array or a pinned torch tensor)."""
+        nb = self.info.node_bytes
+        if out is None:
+            out = np.empty(nb // 8, dtype=np.complex64)
+        ptr, size = _buffer(out)
+        if size != nb:
+            raise ValueError(f"fold_nodes: buffer is {size} B, node region is {nb} B")
+        _check(lib().qsg_engine_fold_nodes(self._h, circuit_text.encode(), ptr, nb))
+        return out
+
+    def load_nodes(self, host_nodes):
+        """Async H2D of a node region on the engine stream (pinned host memory
+        overlaps; keep it alive until the next synchronize)."""
+        ptr, size = _buffer(host_nodes)
+        _check(lib().qsg_engine_load_nodes(self._h, ptr, size))
+        return size
+
+    def export_nodes(self):
+        out = np.empty(self.info.node_bytes // 8, dtype=np.complex64)
+        _check(lib().qsg_engine_export_nodes(self._h, out.ctypes.data, out.nbytes))
+        return out
 
     def run(self, slice_ids, reset: bool = True, per_slice: bool = False):
         ids = np.ascontiguousarray(np.asarray(list(slice_ids), dtype=np.int64))

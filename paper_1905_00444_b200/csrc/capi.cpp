@@ -562,6 +562,18 @@ int qsg_engine_prepare(qsg_engine* e, const int* x1_bits, int n, int64_t* h2d_by
   });
 }
 
+int qsg_engine_fold_nodes(qsg_engine* e, const char* circuit_text, void* host_nodes, int64_t bytes) {
+  return guarded([&] { e->impl->fold_nodes(qsg::parse_circuit(circuit_text), host_nodes, bytes); });
+}
+
+int qsg_engine_load_nodes(qsg_engine* e, const void* host_nodes, int64_t bytes) {
+  return guarded([&] { e->impl->load_nodes(host_nodes, bytes); });
+}
+
+int qsg_engine_export_nodes(qsg_engine* e, void* host_nodes, int64_t bytes) {
+  return guarded([&] { e->impl->export_nodes(host_nodes, bytes); });
+}
+
 int qsg_engine_run(qsg_engine* e, const int64_t* slice_ids, int64_t k, int reset, int per_slice) {
   return guarded([&] { e->impl->run(std::vector<std::int64_t>(slice_ids, slice_ids + k), reset != 0, per_slice != 0); });
 }

@@ -144,9 +144,7 @@ Engine::Engine(const Circuit& c, const ContractionPlan& plan, const EngineOption
   check(cudaMemset(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_)), "acc memset");
   {  // one-time upload of the open fold (x1-independent node tensors)
     std::vector<cfloat> host(static_cast<std::size_t>(node_bytes_ / 8), cfloat{});
-    for (std::size_t q = 0; q < open_fold.nodes.size(); ++q)
-      std::copy(open_fold.nodes[q].data.begin(), open_fold.nodes[q].data.end(),
-                host.begin() + static_cast<std::ptrdiff_t>(node_elem_off_[q]));
+    pack_nodes(open_fold, host.data());
     check(cudaMemcpy(arena_ + bufs_[0].offset, host.data(), static_cast<std::size_t>(node_bytes_), cudaMemcpyHostToDevice),
           "node upload");
   }
@@ -773,6 +771,50 @@ std::int64_t Engine::prepare(const std::vector<int>& x1_bits) {
   for (std::size_t q = 0; q < x1_bits.size(); ++q)
     node_x1_off_[q] = closed_[q] ? x1_bits[q] * node_wire_stride_[q] : 0;
   return 0;  // node tensors are resident; x1 only selects views
+}
+
+namespace {
+bool same_layout(const NetworkShape& a, const NetworkShape& b) {
+  if (a.rows != b.rows || a.cols != b.cols || a.nodes.size() != b.nodes.size() || a.bonds.size() != b.bonds.size() ||
+      a.open_qubits != b.open_qubits)
+    return false;
+  for (std::size_t i = 0; i < a.nodes.size(); ++i)
+    if (a.nodes[i].labels != b.nodes[i].labels || a.nodes[i].dims != b.nodes[i].dims) return false;
+  for (std::size_t i = 0; i < a.bonds.size(); ++i)
+    if (a.bonds[i].label != b.bonds[i].label || a.bonds[i].q0 != b.bonds[i].q0 || a.bonds[i].q1 != b.bonds[i].q1)
+      return false;
+  return true;
+}
+}  // namespace
+
+void Engine::fold_nodes(const Circuit& c, void* host, std::int64_t bytes) const {
+  if (bytes != node_bytes_) throw std::invalid_argument("fold_nodes: buffer size != node_bytes");
+  if (c.num_qubits() != circuit_.num_qubits()) throw std::invalid_argument("fold_nodes: qubit count differs");
+  GridNetwork f = fold_worldlines(c, std::vector<int>(static_cast<std::size_t>(c.num_qubits()), -1));
+  if (!same_layout(f.shape(), shape_)) throw std::invalid_argument("fold_nodes: circuit fold shape differs from the engine's");
+  pack_nodes(f, host);
+}
+
+void Engine::pack_nodes(const GridNetwork& f, void* host) const {
+  cfloat* out = static_cast<cfloat*>(host);
+  std::fill(out, out + node_bytes_ / 8, cfloat{});
+  for (std::size_t q = 0; q < f.nodes.size(); ++q)
+    std::copy(f.nodes[q].data.begin(), f.nodes[q].data.end(), out + node_elem_off_[q]);
+}
+
+void Engine::load_nodes(const void* host, std::int64_t bytes) {
+  if (bytes != node_bytes_) throw std::invalid_argument("load_nodes: size != node_bytes");
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  check(cudaMemcpyAsync(arena_ + bufs_[0].offset, host, static_cast<std::size_t>(bytes), cudaMemcpyHostToDevice, stream_),
+        "node load");
+}
+
+void Engine::export_nodes(void* host, std::int64_t bytes) {
+  if (bytes != node_bytes_) throw std::invalid_argument("export_nodes: size != node_bytes");
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  check(cudaMemcpyAsync(host, arena_ + bufs_[0].offset, static_cast<std::size_t>(bytes), cudaMemcpyDeviceToHost, stream_),
+        "node export");
+  check(cudaStreamSynchronize(stream_), "sync");
 }
 
 void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off, void* per_slice_slot) {

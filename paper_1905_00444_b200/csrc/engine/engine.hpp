@@ -86,6 +86,16 @@ class Engine {
   // H2D byte count (0).
   std::int64_t prepare(const std::vector<int>& x1_bits);
 
+  // Node region (the open fold, node_bytes() of complex64) in host order.
+  // fold_nodes: the open fold of another instance of the same circuit
+  // layout (same grid, depth and CZ pattern, e.g. another gate draw) into
+  // host memory; throws if its fold shape differs.  load_nodes: async H2D
+  // of such a region on the engine stream (pinned host memory overlaps);
+  // later runs use the new circuit instance.  export_nodes: D2H copy.
+  void fold_nodes(const Circuit& c, void* host, std::int64_t bytes) const;
+  void load_nodes(const void* host, std::int64_t bytes);
+  void export_nodes(void* host, std::int64_t bytes);
+
   // Runs the slices in the given order on the engine stream (async).
   // reset: zero the batch accumulator first.  per_slice: keep every
   // slice's contribution (slot i for slice_ids[i]).
@@ -159,6 +169,8 @@ class Engine {
   void launch_ooc_gemm(const Op& op, const std::vector<std::int64_t>& node_off, int* launches);
   void gather_block(const char* src, std::vector<std::int64_t> ext, const std::vector<std::int64_t>& str,
                     std::size_t lo, std::size_t hi, std::int64_t r0, std::int64_t rp, char* dst, int* launches);
+
+  void pack_nodes(const GridNetwork& f, void* host) const;
 
   Circuit circuit_;
   ContractionPlan plan_;

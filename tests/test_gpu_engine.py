@@ -344,3 +344,29 @@ def test_masked_grid_amplitudes_vs_state_vector(gpu):
     assert rel(amps, exact) < 1e-4
     idle_one = np.array([b[6] == "1" for b in bits])
     assert np.all(np.abs(amps[idle_one]) < 1e-7 * np.abs(amps).max())
+
+
+def test_load_nodes_rebinds_circuit_instance(gpu, cases):
+    """Another gate draw of the same layout through fold_nodes + load_nodes
+    gives bit-identical amplitudes to a fresh engine on that circuit; a
+    different layout is rejected."""
+    import torch
+    _, meta = cases
+    case = meta["cases"][0]
+    a = gpu.generate_rqc(case["rows"], case["cols"], case["m"], case["seed"])
+    b = gpu.generate_rqc(case["rows"], case["cols"], case["m"], case["seed"] + 17)
+    with gpu.Engine(b, case["plan"]) as fresh:
+        want_bits, want = fresh.amplitude_batch(case["x1"], range(case["slices"]))
+    with gpu.Engine(a, case["plan"]) as e:
+        assert np.array_equal(e.export_nodes(), e.fold_nodes(a))
+        host = torch.empty(e.info.node_bytes // 8, dtype=torch.complex64, pin_memory=True)
+        e.fold_nodes(b, out=host)
+        assert e.load_nodes(host) == e.info.node_bytes
+        bits, got = e.amplitude_batch(case["x1"], range(case["slices"]))
+        assert bits == want_bits and np.array_equal(got, want)
+        assert np.array_equal(e.export_nodes(), host.numpy())
+        other = gpu.generate_rqc(case["rows"], case["cols"], case["m"] + 1, case["seed"])
+        with pytest.raises(gpu.QsgError):
+            e.fold_nodes(other)
+        with pytest.raises(gpu.QsgError):
+            e.load_nodes(np.zeros(4, dtype=np.complex64))
