@@ -207,6 +207,78 @@ __global__ void __launch_bounds__(NT) splitk_reduce_kernel(const KParams p, int 
   }
 }
 
+// Narrow-N variant (n <= 16): the 64 x 128 tile above wastes 7/8 of its
+// FFMAs and stores on n = 16 (the bond-closing steps of the column sweeps,
+// e.g. m = 2^20 x n = 16 x k = 16 with A in T layout).  Here a thread owns
+// one output row and all n columns: A is staged per 32-k chunk through
+// shared memory with coalesced loads (T layout: along m; N layout: along k),
+// B's chunk (<= 32 x 16) is broadcast from shared memory, and each thread
+// stores its contiguous row.  HBM-bound: 8 (m k + m n) bytes per launch.
+constexpr int NR = 128, NKC = 32, NNW = 16;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NR) cgemm_narrow_kernel(const KParams p) {
+  __shared__ float2 As[NKC][NR + 1];
+  __shared__ float2 Bs[NKC][NNW];
+  const int tid = threadIdx.x;
+  const long long m0 = static_cast<long long>(blockIdx.x) * NR;
+  const long long M = p.m, N = p.n, K = p.k;
+  float2 acc[NNW];
+#pragma unroll
+  for (int j = 0; j < NNW; ++j) acc[j] = make_float2(0.f, 0.f);
+  for (long long k0 = 0; k0 < K; k0 += NKC) {
+    const int kc = static_cast<int>(min(static_cast<long long>(NKC), K - k0));
+#pragma unroll 4
+    for (int i = 0; i < NKC; ++i) {
+      const int idx = tid + i * NR;
+      int r, kk;
+      if (TA) { kk = idx / NR; r = idx % NR; } else { r = idx / NKC; kk = idx % NKC; }
+      const long long gm = m0 + r;
+      As[kk][r] = (gm < M && kk < kc) ? (TA ? p.a[(k0 + kk) * M + gm] : p.a[gm * K + k0 + kk]) : make_float2(0.f, 0.f);
+    }
+    for (int idx = tid; idx < NKC * NNW; idx += NR) {
+      const int kk = idx / NNW, j = idx % NNW;
+      Bs[kk][j] = (kk < kc && j < N) ? (TB ? p.b[j * K + k0 + kk] : p.b[(k0 + kk) * N + j]) : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kc; ++kk) {
+      const float2 a = As[kk][tid];
+#pragma unroll
+      for (int j = 0; j < NNW; ++j) cfma(acc[j], a, Bs[kk][j]);
+    }
+    __syncthreads();
+  }
+  const int sa = pending_shift(p.meta_a, p.norm_a), sb = pending_shift(p.meta_b, p.norm_b);
+  const int shift = sa + sb;
+  float local = 0.f;
+  const long long gm = m0 + tid;
+  if (gm < M) {
+#pragma unroll
+    for (int j = 0; j < NNW; ++j) {
+      const float2 v = make_float2(scalbnf(acc[j].x, -shift), scalbnf(acc[j].y, -shift));
+      acc[j] = v;
+      local = fmaxf(local, v.x * v.x + v.y * v.y);
+    }
+    if (N == NNW) {
+      float4* row = reinterpret_cast<float4*>(p.c + gm * N);
+#pragma unroll
+      for (int j = 0; j < NNW; j += 2) row[j / 2] = make_float4(acc[j].x, acc[j].y, acc[j + 1].x, acc[j + 1].y);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NNW; ++j)
+        if (j < N) p.c[gm * N + j] = acc[j];
+    }
+  }
+  if (p.meta_c) {
+    for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+    if ((tid & 31) == 0 && local > 0.f) atomicMax(&p.meta_c->maxsq_bits, __float_as_uint(local));
+    if (blockIdx.x == 0 && tid == 0)
+      p.meta_c->log_scale = (p.meta_a ? p.meta_a->log_scale : 0.0) + (p.meta_b ? p.meta_b->log_scale : 0.0) + shift;
+  }
+}
+
+bool use_narrow(std::int64_t m, std::int64_t n) { return n <= NNW && m >= 1024; }
+
 int sm_count() {
   static int n = [] {
     int dev = 0, v = 148;
@@ -229,6 +301,7 @@ int choose_splits(std::int64_t m, std::int64_t n, std::int64_t k) {
 }  // namespace
 
 std::int64_t cgemm_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
+  if (use_narrow(m, n)) return 0;
   const int s = choose_splits(m, n, k);
   return s > 1 ? static_cast<std::int64_t>(s) * m * n * 8 : 0;
 }
@@ -248,6 +321,20 @@ cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches) {
   p.meta_c = g.meta_c;
   p.norm_a = g.norm_a;
   p.norm_b = g.norm_b;
+  if (use_narrow(g.m, g.n) && g.k > 0) {
+    const std::int64_t blocks = (g.m + NR - 1) / NR;
+    if (blocks > 0x7fffffff) throw std::length_error("cgemm: m too large for the grid");
+    const dim3 grid(static_cast<unsigned>(blocks));
+    if (g.trans_a) {
+      if (g.trans_b) cgemm_narrow_kernel<true, true><<<grid, NR, 0, stream>>>(p);
+      else cgemm_narrow_kernel<true, false><<<grid, NR, 0, stream>>>(p);
+    } else {
+      if (g.trans_b) cgemm_narrow_kernel<false, true><<<grid, NR, 0, stream>>>(p);
+      else cgemm_narrow_kernel<false, false><<<grid, NR, 0, stream>>>(p);
+    }
+    if (launches) ++*launches;
+    return cudaGetLastError();
+  }
   int splits = choose_splits(g.m, g.n, g.k);
   if (splits > 1 && (g.workspace == nullptr || g.workspace_bytes < cgemm_workspace_bytes(g.m, g.n, g.k))) splits = 1;
   std::int64_t kchunk = g.k;

@@ -831,7 +831,8 @@ struct Tc5Cfg {
   static constexpr int B_B = (BN / 2) * KB * 2;  // one fp16 plane of this CTA's half of B_r^T
   static constexpr int STAGE_BYTES = A_B + 2 * B_B;
   static constexpr int EPI_PITCH = 20;
-  static constexpr int EPI_BYTES = (kWorkers / 32) * 32 * EPI_PITCH * 4;
+  // + per worker warp a 32-entry table of its rows' permuted offsets
+  static constexpr int EPI_BYTES = (kWorkers / 32) * 32 * (EPI_PITCH * 4 + 8);
   static constexpr int STAGES =
       ((224 * 1024 - EPI_BYTES) / STAGE_BYTES) > 6 ? 6 : ((224 * 1024 - EPI_BYTES) / STAGE_BYTES);
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
@@ -1085,9 +1086,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // Fused output permutation: the column part of a float4's offset is
     // f(c0 / 2) + f(2 * (lane & 3)) (disjoint bits of the complex column).
     long long lane_col_off = 0;
+    // Fused permutation: per-warp table of the stored rows' offsets.
+    long long* const row_tab =
+        reinterpret_cast<long long*>(epi_stage + (kWorkers / 32) * 32 * Cfg::EPI_PITCH) + (warp - 2) * 32;
     if (p.store_perm)
       for (int b = 0; b < 3 && b < p.ncol_bits; ++b)
         if (((2 * (lane & 3)) >> b) & 1) lane_col_off += 1ll << p.col_pos[b];
+    auto col_bit = [&](int b) { return p.ncol_bits > b ? 1ll << p.col_pos[b] : 0ll; };
+    // sum_b bit_b(x) << pos[b] over the warp's lanes (distinct bit positions:
+    // the sum is an OR, reduced as two 32-bit halves).
+    auto warp_bits = [&](long long x, int pos_lo, int pos_hi) {
+      unsigned long long t = 0;
+      if (pos_lo >= 0 && ((x >> lane) & 1)) t |= 1ull << pos_lo;
+      if (pos_hi >= 0 && ((x >> (lane + 32)) & 1)) t |= 1ull << pos_hi;
+      const unsigned lo = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(t));
+      const unsigned hi = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(t >> 32));
+      return static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo);
+    };
     float local = 0.f;
     int s = 0;
     uint32_t ph = 0;
@@ -1149,13 +1164,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           float* stg = epi_stage + (warp - 2) * 32 * Cfg::EPI_PITCH;
           long long my_row_off = 0, col_tile_off = 0;
           if (p.store_perm) {
-            const long long grow = row_base + lane;
-            for (int b = 0; b < p.nrow_bits; ++b)
-              if ((grow >> b) & 1) my_row_off += 1ll << p.row_pos[b];
+            // row_base is a multiple of 32: its bits and the lane's are
+            // disjoint.  Lane b reduces bit b (and b + 32); the positions are
+            // re-read per tile (not kept in registers next to acc[]).
+            const int rp0 = lane < p.nrow_bits ? p.row_pos[lane] : -1;
+            const int rp1 = lane + 32 < p.nrow_bits ? p.row_pos[lane + 32] : -1;
+            const int cpl = lane < p.ncol_bits ? p.col_pos[lane] : -1;
+            my_row_off = warp_bits(row_base, rp0, rp1);
+            for (int b = 0; b < 5 && b < p.nrow_bits; ++b)
+              if ((lane >> b) & 1) my_row_off += 1ll << p.row_pos[b];
             const long long gcol = (static_cast<long long>(n_tile) * kPairBN + half * HALF) / 2;
-            for (int b = 0; b < p.ncol_bits; ++b)
-              if ((gcol >> b) & 1) col_tile_off += 1ll << p.col_pos[b];
+            col_tile_off = warp_bits(gcol, cpl, -1);
           }
+          // The rows' offsets, read back per store (no shuffles, no registers).
+          if (p.store_perm) row_tab[lane] = my_row_off + col_tile_off;
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += 16) {
 #pragma unroll
@@ -1170,23 +1192,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
             }
             __syncwarp();
-            long long jc_off = lane_col_off;
-            if (p.store_perm) {
-              const int jhi = c0 >> 1;  // multiple of 8: column bits 3..6
-#pragma unroll
-              for (int b = 3; b < 7; ++b)
-                if (b < p.ncol_bits && ((jhi >> b) & 1)) jc_off += 1ll << p.col_pos[b];
-            }
+            // column bits 3..5 of this 8-complex run (c0 < HALF <= 128: jhi < 64)
+            const long long jc =
+                ((c0 >> 4) & 1 ? col_bit(3) : 0ll) + ((c0 >> 5) & 1 ? col_bit(4) : 0ll) + ((c0 >> 6) & 1 ? col_bit(5) : 0ll);
             if (p.c_split) {
               // Split output, 4 complex per lane: one 16-byte hi and one
               // 16-byte lo store (half the store instructions of 2 complex).
-              long long jc = 0;  // column bits 3..6 of this 8-complex run
-              if (p.store_perm) {
-                const int jhi = c0 >> 1;
-#pragma unroll
-                for (int b = 3; b < 7; ++b)
-                  if (b < p.ncol_bits && ((jhi >> b) & 1)) jc += 1ll << p.col_pos[b];
-              }
 #pragma unroll
               for (int it = 0; it < 2; ++it) {
                 const int r = it * 16 + (lane >> 1), hf = lane & 1;
@@ -1194,8 +1205,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float4 v1 = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 8 * hf + 4);
                 long long o;  // complex offset of v0.xy (col bits 0..2 are the output's bits 0..2)
                 if (p.store_perm) {
-                  const long long ro = __shfl_sync(0xffffffffu, my_row_off, r);
-                  o = ro + col_tile_off + jc + 4 * hf;
+                  o = row_tab[r] + jc + 4 * hf;
                 } else {
                   o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 8 * hf) >> 1;
                 }
@@ -1225,8 +1235,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const float4 v = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 4 * c4);
               long long o;  // complex offset of v.xy in C
               if (p.store_perm) {
-                const long long ro = __shfl_sync(0xffffffffu, my_row_off, r);
-                o = ro + col_tile_off + jc_off;
+                o = row_tab[r] + jc + lane_col_off;
               } else {
                 o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) >> 1;
               }

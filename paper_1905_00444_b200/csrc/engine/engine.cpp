@@ -955,6 +955,14 @@ void Engine::reset_profile() {
 }
 
 std::string Engine::describe() const {
+  // "[r0 r1 ... | c0 c1 ...]": output bit positions of the GEMM row / column bits.
+  auto perm_text = [](const Op& op) {
+    std::string t = " [";
+    for (int b = 0; b < op.nrow_bits; ++b) t += std::to_string(op.row_pos[b]) + " ";
+    t += "|";
+    for (int b = 0; b < op.ncol_bits; ++b) t += " " + std::to_string(op.col_pos[b]);
+    return t + "]";
+  };
   std::ostringstream os;
   os << "arena " << arena_bytes_ << " B, nodes " << node_bytes_ << " B, ops " << ops_.size();
   if (host_arena_bytes_ > 0)
@@ -966,7 +974,8 @@ std::string Engine::describe() const {
     else if (op.kind == 1)
       os << "  gemm    step " << op.step << " m " << op.m << " n " << op.n << " k " << op.k << " flops " << op.flops
          << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes
-         << (op.store_perm ? " fused-store" : "") << (op.c_split ? " split-out" : "")
+         << (op.store_perm ? " fused-store" : "") << (op.store_perm ? perm_text(op) : std::string())
+         << (op.c_split ? " split-out" : "")
          << (op.a_presplit ? " split-in" : "")
          << (op.ooc ? " ooc pieces " + std::to_string(op.pieces.size()) : std::string()) << "\n";
     else os << "  accumulate " << op.count << "\n";
