@@ -845,7 +845,12 @@ struct Tc5Cfg {
 // both CTAs' TMA loads complete on the leader's full[s] (cta_group::2) and
 // the worker warps only promote and store.  map_a is then the A_hi plane
 // and map_alo the A_lo plane (64 or 32 fp16 per row per stage: SW128 or SW64).
-template <int kPairBN, bool kSplitA, int kBK = BK16>
+// kDirect: single-chunk tiles (k <= 64): no promotion registers; the
+// epilogue reads each 16-column slab straight from TMEM and frees the
+// accumulator buffer after the tile's stores (the MMA meanwhile fills the
+// other buffer).  Without the 128 promoted floats per thread the worker
+// warps run spill-free.
+template <int kPairBN, bool kSplitA, int kBK = BK16, bool kDirect = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_alo,
                           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -1053,9 +1058,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    float acc[HALF];
+    float acc[kDirect ? 1 : HALF];
 #pragma unroll
-    for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+    for (int i = 0; i < (kDirect ? 1 : HALF); ++i) acc[i] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
     const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
     const int ea = p.a_presplit ? p.meta_a->split_exp : f16_exp(p.meta_a), eb = f16_exp(p.meta_b);
@@ -1145,17 +1150,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int buf = static_cast<int>(qq & 1);
         mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if constexpr (!kDirect) {
 #pragma unroll
-        for (int j = 0; j < HALF / 16; ++j) {
-          float v[16];
-          tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + 16 * j), v);
+          for (int j = 0; j < HALF / 16; ++j) {
+            float v[16];
+            tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + 16 * j), v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
+            for (int i = 0; i < 16; ++i) acc[16 * j + i] += v[i];
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[buf]);
-        if (qq % nchunks == nchunks - 1) {
+        if (kDirect || qq % nchunks == nchunks - 1) {
           long long m_pair;
           int n_tile;
           pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
@@ -1180,15 +1187,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (p.store_perm) row_tab[lane] = my_row_off + col_tile_off;
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += 16) {
+            float a16[16];
+            if constexpr (kDirect) {
+              tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0), a16);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) a16[i] = acc[c0 + i];
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-              float4 v = make_float4(acc[c0 + 4 * i] * f1, acc[c0 + 4 * i + 1] * f1, acc[c0 + 4 * i + 2] * f1,
-                                     acc[c0 + 4 * i + 3] * f1);
+              float4 v = make_float4(a16[4 * i] * f1, a16[4 * i + 1] * f1, a16[4 * i + 2] * f1, a16[4 * i + 3] * f1);
               if (u2 != 0) { v.x *= f2; v.y *= f2; v.z *= f2; v.w *= f2; }
               local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
               if (p.c_split)
-                v = make_float4(acc[c0 + 4 * i] * fy, acc[c0 + 4 * i + 1] * fy, acc[c0 + 4 * i + 2] * fy,
-                                acc[c0 + 4 * i + 3] * fy);
+                v = make_float4(a16[4 * i] * fy, a16[4 * i + 1] * fy, a16[4 * i + 2] * fy, a16[4 * i + 3] * fy);
               *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
             }
             __syncwarp();
@@ -1244,8 +1256,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
           }
+          if constexpr (kDirect) {
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+          } else {
 #pragma unroll
-          for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+            for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
+          }
         }
       }
     }
@@ -1582,13 +1599,25 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                          Tc5Cfg<BN>::SMEM);
     return resident_pairs(cgemm_f16_pair_kernel<BN, false>, Tc5Cfg<BN>::SMEM);
   }();
+  static const bool attrs_direct = [] {
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN>::SMEM);
+    return true;
+  }();
+  (void)attrs_direct;
   const long long clusters = std::min<long long>(pairs, slots);
-  if (split)
-    cgemm_f16_pair_kernel<BN, true>
-        <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  const unsigned grid = static_cast<unsigned>(2 * clusters);
+  const bool direct = p.kblocks <= p.chunk && !(std::getenv("QSG_TC_DIRECT") && std::getenv("QSG_TC_DIRECT")[0] == '0');
+  if (direct && split)
+    cgemm_f16_pair_kernel<BN, true, BK16, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  else if (direct)
+    cgemm_f16_pair_kernel<BN, false, BK16, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  else if (split)
+    cgemm_f16_pair_kernel<BN, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else
-    cgemm_f16_pair_kernel<BN, false>
-        <<<static_cast<unsigned>(2 * clusters), kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    cgemm_f16_pair_kernel<BN, false><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   return cudaGetLastError();
 }
 
