@@ -299,6 +299,9 @@ def run_ours(args):
     text = Q.generate_rqc(r, c, m, s)
     plan_text = open(os.path.join(ROOT, cfg["plan"])).read()
     plan = json.loads(plan_text)
+    rewrites = None
+    if args.reassociate:
+        plan_text, rewrites = Q.reassociate_plan(text, plan_text)
     open_q = plan["open_qubits"]
     n = r * c
     xb = args.x1_batch if args.x1_batch is not None else cfg.get("x1_batch", 1)
@@ -472,7 +475,10 @@ def run_ours(args):
                               "event windows" if small else
                               f"working set ({info.arena_bytes / 2**30:.1f} GiB arena) >> 126 MB L2; no flush needed"),
                        "arena_bytes": info.arena_bytes, "tensor_cores": not args.no_tc,
-                       **({"memory_budget": args.memory_budget} if args.memory_budget else {})},
+                       **({"memory_budget": args.memory_budget} if args.memory_budget else {}),
+                       **({"plan": f"reassociated ({rewrites} tree rewrites; Eq.1 flops/slice "
+                                   f"{info.flops_per_slice:.4g} vs the plan's {plan['per_slice']['flops']:.4g})"}
+                          if rewrites is not None else {})},
             "tflops_eq1": tflops, "tflops_frac_fp32_simt": tflops / fp32_peak,
             "e2e": {"value": e2e_value, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "note": "per step: H2D of the circuit's node tensors (host open fold, pinned) + host x1 "
@@ -521,6 +527,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="2",
                     help="BASELINE config: 1, 2 (default, the metric's workload), 3/4 (Bristlecone stand-ins), 5")
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
+    ap.add_argument("--reassociate", action="store_true",
+                    help="opt-in contraction-tree rewrite of the plan (Q.reassociate_plan); off for the headline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-out", default="", help="write the per-op profile (one JSON line per op) here")
     ap.add_argument("--x1-batch", type=int, default=None,

@@ -255,6 +255,14 @@ int qsg_amplitude_batch(qsg_engine* e, const int* x1_bits, int n, const int64_t*
  * (re, im) and bitstrings, each draw in the reference's batch order. */
 int qsg_widen_plan(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
                    const int* extra_open, int nextra, char* buf, int64_t cap, int64_t* len);
+/* Contraction-tree rewrite (no reference counterpart; opt-in planner pass
+ * over plans loaded like qsg_plan_json, src/plan.cpp:508-552): a step output
+ * T = A x B read once by U = T x C becomes W = B x C, U = A x W (or A, B
+ * swapped) when that cuts the pair's Eq.(1) flops by >= 25% without a larger
+ * intermediate, to a fixed point.  Same cut, slices and amplitudes (up to
+ * rounding); JSON out, *rewrites = number of rewrites. */
+int qsg_reassociate_plan(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                         char* buf, int64_t cap, int64_t* len, int* rewrites);
 int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
                           const int64_t* slice_ids, int64_t k, double* amps_host, char* bitstrings_host);
 

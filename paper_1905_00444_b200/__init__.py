@@ -146,6 +146,7 @@ def lib():
         "qsg_engine_set_profile": (i32, [vp, i32]),
         "qsg_amplitude_batch": (i32, [vp, P(i32), i32, P(i64), i64, dp, cp]),
         "qsg_widen_plan": (i32, [cp, i32, cp, P(i32), i32, P(i32), i32, cp, i64, P(i64)]),
+        "qsg_reassociate_plan": (i32, [cp, i32, cp, P(i32), i32, cp, i64, P(i64), P(i32)]),
         "qsg_amplitude_batches": (i32, [vp, P(i32), i32, P(i32), i32, i32, P(i64), i64, dp, cp]),
         "qsg_run_amplitudes": (i32, [vp, cp, i32, i32, i64, i64, u64, dp, P(i64), P(u64)]),
         "qsg_sample": (i32, [vp, i64, i64, i64, i32, C.c_double, u64, cp, dp, P(_SampleStats), P(_XebReport)]),
@@ -370,6 +371,21 @@ def widen_plan(circuit_text: str, plan_text: str, extra_open, kind: int = PLAN_J
     a, p = _i32(open_qubits)
     e, pe = _i32(extra_open)
     return _text(lib().qsg_widen_plan, circuit_text.encode(), kind, plan_text.encode(), p, len(a), pe, len(e))
+
+
+def reassociate_plan(circuit_text: str, plan_text: str = "", kind: int = PLAN_JSON, open_qubits=()):
+    """Opt-in contraction-tree rewrite (no reference counterpart): (A x B) x C
+    -> A x (B x C) where that cuts the pair's Eq.(1) flops by >= 25% without a
+    larger intermediate, to a fixed point.  Returns (plan JSON, rewrites);
+    same cut, slices and amplitudes up to rounding."""
+    a, p = _i32(open_qubits)
+    r = C.c_int(0)
+    n = C.c_int64(0)
+    args = (circuit_text.encode(), kind, plan_text.encode(), p, len(a))
+    _check(lib().qsg_reassociate_plan(*args, None, 0, C.byref(n), C.byref(r)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().qsg_reassociate_plan(*args, buf, n.value + 1, C.byref(n), C.byref(r)))
+    return buf.value.decode(), r.value
 
 
 def xeb_score(n: int, probs, hog_median=None) -> dict:

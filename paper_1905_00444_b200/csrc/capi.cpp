@@ -641,6 +641,17 @@ int qsg_widen_plan(const char* circuit_text, int kind, const char* plan_text, co
   });
 }
 
+int qsg_reassociate_plan(const char* circuit_text, int kind, const char* plan_text, const int* open, int nopen,
+                         char* buf, int64_t cap, int64_t* len, int* rewrites) {
+  return guarded([&] {
+    const qsg::Circuit c = qsg::parse_circuit(circuit_text);
+    const qsg::ContractionPlan plan = make_plan(c, kind, plan_text, std::vector<int>(open, open + nopen), 0);
+    int r = 0;
+    put_text(qsg::plan_to_json(qsg::reassociate_plan(qsg::fold_shape(c, plan.open_qubits), plan, &r)), buf, cap, len);
+    if (rewrites) *rewrites = r;
+  });
+}
+
 int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
                           const int64_t* slice_ids, int64_t k, double* amps_host, char* bitstrings_host) {
   return guarded([&] {

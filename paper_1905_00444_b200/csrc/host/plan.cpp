@@ -238,6 +238,74 @@ void annotate_plan(const NetworkShape& shape, ContractionPlan& plan) {
   if (plan.peak_memory == 0) plan.peak_memory = live_bytes;
 }
 
+ContractionPlan reassociate_plan(const NetworkShape& shape, const ContractionPlan& in, int* rewrites) {
+  ContractionPlan p = in;
+  annotate_plan(shape, p);
+  const NetworkShape sliced = sliced_shape(shape, p.cut);
+  auto flops_of = [](const TensorShape& a, const TensorShape& b, const TensorShape& o) {
+    return std::exp2(3.0 + 0.5 * (log2_volume(a) + log2_volume(b) + log2_volume(o)));
+  };
+  int count = 0, fresh = 0;
+  for (bool changed = true; changed;) {
+    changed = false;
+    std::map<std::string, TensorShape> shp;
+    for (std::size_t q = 0; q < sliced.nodes.size(); ++q) shp[node_name(static_cast<int>(q))] = sliced.nodes[q];
+    for (const auto& st : p.steps) shp[st.out] = sorted_shape(merge_free(shp.at(st.lhs), shp.at(st.rhs)));
+    for (std::size_t i = 0; i < p.steps.size() && !changed; ++i) {
+      const PlanStep& si = p.steps[i];
+      std::size_t j = i + 1;
+      while (j < p.steps.size() && p.steps[j].lhs != si.out && p.steps[j].rhs != si.out) ++j;
+      if (j == p.steps.size()) continue;  // the final tensor
+      const std::string c = p.steps[j].lhs == si.out ? p.steps[j].rhs : p.steps[j].lhs;
+      const TensorShape& T = shp.at(si.out);
+      const TensorShape& U = shp.at(p.steps[j].out);
+      const double old_cost = flops_of(shp.at(si.lhs), shp.at(si.rhs), T) + flops_of(T, shp.at(c), U);
+      double best = old_cost;
+      std::string keep, join;
+      for (int side = 0; side < 2; ++side) {
+        const std::string& x = side == 0 ? si.lhs : si.rhs;  // stays, meets W last
+        const std::string& y = side == 0 ? si.rhs : si.lhs;  // joins c first
+        const TensorShape W = sorted_shape(merge_free(shp.at(y), shp.at(c)));
+        if (log2_volume(W) > std::max(log2_volume(T), log2_volume(U))) continue;  // no larger intermediates
+        const double cost = flops_of(shp.at(y), shp.at(c), W) + flops_of(shp.at(x), W, U);
+        if (cost < best) {
+          best = cost;
+          keep = x;
+          join = y;
+        }
+      }
+      if (keep.empty() || best > 0.75 * old_cost) continue;
+      PlanStep w, u;
+      w.out = "r" + std::to_string(fresh++);
+      w.lhs = join;
+      w.rhs = c;
+      u.out = p.steps[j].out;
+      u.lhs = keep;
+      u.rhs = w.out;
+      p.steps[j] = u;
+      p.steps.insert(p.steps.begin() + static_cast<std::ptrdiff_t>(j), w);
+      p.steps.erase(p.steps.begin() + static_cast<std::ptrdiff_t>(i));
+      ++count;
+      changed = true;
+    }
+  }
+  // Positional names, as plan_from_json assigns them.
+  std::map<std::string, std::string> rename;
+  for (std::size_t i = 0; i < p.steps.size(); ++i) rename[p.steps[i].out] = step_name(static_cast<int>(i));
+  auto ren = [&](const std::string& n) {
+    auto it = rename.find(n);
+    return it == rename.end() ? n : it->second;
+  };
+  for (auto& st : p.steps) {
+    st.lhs = ren(st.lhs);
+    st.rhs = ren(st.rhs);
+    st.out = ren(st.out);
+  }
+  annotate_plan(shape, p);
+  if (rewrites) *rewrites = count;
+  return p;
+}
+
 namespace {
 
 // Greedy pairing by (result volume, Eq.1 flops, lexicographic names);

@@ -177,6 +177,14 @@ GridNetwork apply_cut(const GridNetwork& net, const Cut& cut, std::int64_t slice
 
 void annotate_plan(const NetworkShape& shape, ContractionPlan& plan);
 ContractionPlan plan_contraction(const NetworkShape& shape, const PlanOptions& opts = {});
+// Contraction-tree rewrite (not in the reference; opt-in): T = A x B read
+// once by U = T x C becomes W = B x C, U = A x W (or with A and B swapped)
+// when that cuts the pair's Eq.(1) flops by >= 25% without a larger
+// intermediate, repeated to a fixed point.  Collapses chains that expand a
+// tensor by a small node and contract the expansion with the next small
+// node (X.(Y.Z) for (X.Y).Z).  Same amplitudes up to rounding, same cut and
+// slices; outputs renamed positionally.
+ContractionPlan reassociate_plan(const NetworkShape& shape, const ContractionPlan& plan, int* rewrites = nullptr);
 std::string plan_to_json(const ContractionPlan& plan);
 ContractionPlan plan_from_json(const std::string& text, const NetworkShape& shape);
 std::vector<int> plan_json_open_qubits(const std::string& text);

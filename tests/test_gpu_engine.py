@@ -370,3 +370,26 @@ def test_load_nodes_rebinds_circuit_instance(gpu, cases):
             e.fold_nodes(other)
         with pytest.raises(gpu.QsgError):
             e.load_nodes(np.zeros(4, dtype=np.complex64))
+
+
+@pytest.mark.parametrize("tc", [True, False])
+def test_reassociated_plan_same_amplitudes(gpu, tc, monkeypatch):
+    """A sweep plan and its reassociated tree give the same batch (1e-5) and
+    both match the double state vector (1e-4)."""
+    import qsim_oracle as O
+    from test_program import _sweep_plan
+    if tc:
+        monkeypatch.setenv("QSG_TC_MIN_FLOPS", "0")
+    text, plan, opn = _sweep_plan(4, 5, 16, 3, 4)
+    new, k = gpu.reassociate_plan(text, plan)
+    assert k > 0
+    x1 = [-1 if q in opn else (q * 5 + 1) % 2 for q in range(20)]
+    with gpu.Engine(text, plan, tensor_cores=tc) as e:
+        bits, want = e.amplitude_batch(x1, [0])
+    with gpu.Engine(text, new, tensor_cores=tc) as e:
+        bits2, got = e.amplitude_batch(x1, [0])
+    assert bits == bits2
+    assert rel(got, want) < 1e-5
+    sv = O.evolve(text)
+    exact = np.array([sv[int(b, 2)] for b in bits])
+    assert rel(got, exact) < 1e-4

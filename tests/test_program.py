@@ -67,3 +67,36 @@ def test_out_of_core_automatic_budget():
         head = Q.program_listing(text, plan, memory_budget=-1, device_memory=dev).splitlines()[0].split()
         arena, slot = int(head[1]), int(head[head.index("scratch") + 1])
         assert arena + 2 * slot <= 0.92 * dev
+
+
+def _sweep_plan(rows, cols, m, seed, nopen):
+    """Column-major sweep chained onto one accumulator (the config 3/4 plan shape)."""
+    text = Q.generate_rqc(rows, cols, m, seed)
+    nodes = [r * cols + c for c in range(cols) for r in range(rows)]
+    order, acc = [], f"n_{nodes[0]:03d}"
+    for i, q in enumerate(nodes[1:]):
+        order.append([acc, f"n_{q:03d}"])
+        acc = f"s{i:03d}"
+    opn = sorted((rows - 1) * cols + c for c in range(nopen))
+    draft = {"version": 1, "open_qubits": opn, "cut": {"labels": [], "group": 1}, "order": order}
+    return text, Q.plan_json(text, opn, Q.PLAN_JSON, json.dumps(draft)), opn
+
+
+def test_reassociate_plan_sweeps():
+    """The opt-in tree rewrite keeps cut, slices, open qubits and peak bounds,
+    lowers the Eq.(1) flops of sweep plans, and is idempotent."""
+    text, plan, _ = _sweep_plan(4, 5, 16, 3, 4)
+    new, k = Q.reassociate_plan(text, plan)
+    a, b = json.loads(plan), json.loads(new)
+    assert k > 0 and len(b["order"]) == len(a["order"])
+    assert b["per_slice"]["flops"] < 0.6 * a["per_slice"]["flops"]
+    assert b["per_slice"]["max_rank"] <= a["per_slice"]["max_rank"]
+    assert Q.reassociate_plan(text, new)[1] == 0
+    c3 = Q.generate_rqc(6, 10, 32, 0)
+    p3 = open(os.path.join(ROOT, "configs", "config3_standin_6x10_plan.json")).read()
+    n3, k3 = Q.reassociate_plan(c3, p3)
+    a3, b3 = json.loads(p3), json.loads(n3)
+    assert k3 > 0 and b3["slices"] == a3["slices"] and b3["cut"] == a3["cut"]
+    assert b3["per_slice"]["flops"] < a3["per_slice"]["flops"]
+    assert b3["per_slice"]["peak_memory"] <= a3["per_slice"]["peak_memory"]
+    assert "gemm" in Q.program_listing(c3, n3)
