@@ -830,11 +830,15 @@ struct Tc5Cfg {
   static constexpr int A_B = BM * KB * 4;        // raw fp32 A tile (= A hi + lo fp16 planes)
   static constexpr int B_B = (BN / 2) * KB * 2;  // one fp16 plane of this CTA's half of B_r^T
   static constexpr int STAGE_BYTES = A_B + 2 * B_B;
-  static constexpr int EPI_PITCH = 20;
-  // + per worker warp a 32-entry table of its rows' permuted offsets
-  static constexpr int EPI_BYTES = (kWorkers / 32) * 32 * (EPI_PITCH * 4 + 8);
+  static constexpr int EPI_PITCH = 20;  // fp32 / narrow path: 16-column slabs, padded rows
+  // Per worker warp: a 32 x 32-float staging slab (split path: XOR-swizzled
+  // 16-byte chunks, no padding) + a 32-entry table of its rows' permuted
+  // offsets (32-bit, in units of 8 complex: rows never land on output bits 0..2).
+  static constexpr int EPI_WARP_FLOATS = 32 * 32;
+  static constexpr int EPI_BYTES = (kWorkers / 32) * (EPI_WARP_FLOATS * 4 + 32 * 4);
+  static constexpr int SMEM_CAP = 232448 - 1024 - 256;  // 227 KiB opt-in minus alignment slack and barriers
   static constexpr int STAGES =
-      ((224 * 1024 - EPI_BYTES) / STAGE_BYTES) > 6 ? 6 : ((224 * 1024 - EPI_BYTES) / STAGE_BYTES);
+      ((SMEM_CAP - EPI_BYTES) / STAGE_BYTES) > 6 ? 6 : ((SMEM_CAP - EPI_BYTES) / STAGE_BYTES);
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
   static_assert(STAGES >= 2, "shared memory budget");
@@ -1092,8 +1096,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // f(c0 / 2) + f(2 * (lane & 3)) (disjoint bits of the complex column).
     long long lane_col_off = 0;
     // Fused permutation: per-warp table of the stored rows' offsets.
-    long long* const row_tab =
-        reinterpret_cast<long long*>(epi_stage + (kWorkers / 32) * 32 * Cfg::EPI_PITCH) + (warp - 2) * 32;
+    uint32_t* const row_tab =
+        reinterpret_cast<uint32_t*>(epi_stage + (kWorkers / 32) * Cfg::EPI_WARP_FLOATS) + (warp - 2) * 32;
     if (p.store_perm)
       for (int b = 0; b < 3 && b < p.ncol_bits; ++b)
         if (((2 * (lane & 3)) >> b) & 1) lane_col_off += 1ll << p.col_pos[b];
@@ -1168,7 +1172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
           const long long row_base = m_pair * 256 + static_cast<long long>(rank) * BM + quad * 32;
           float* base = p.c + row_base * p.n2 + static_cast<long long>(n_tile) * kPairBN + half * HALF;
-          float* stg = epi_stage + (warp - 2) * 32 * Cfg::EPI_PITCH;
+          float* stg = epi_stage + (warp - 2) * Cfg::EPI_WARP_FLOATS;
           long long my_row_off = 0, col_tile_off = 0;
           if (p.store_perm) {
             // row_base is a multiple of 32: its bits and the lane's are
@@ -1184,7 +1188,84 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             col_tile_off = warp_bits(gcol, cpl, -1);
           }
           // The rows' offsets, read back per store (no shuffles, no registers).
-          if (p.store_perm) row_tab[lane] = my_row_off + col_tile_off;
+          if (p.store_perm) row_tab[lane] = static_cast<uint32_t>((my_row_off + col_tile_off) >> 3);
+          bool stored = false;
+          if constexpr (HALF >= 32 && kDirect) {
+            if (p.c_split) {
+              // Split output in 32-column slabs: lane = row stages 32 floats
+              // (chunk c of row r at 16-byte slot c ^ (r & 7): conflict-free
+              // both ways), then 4 lanes per row convert 4 complex each and
+              // store 64-byte runs per plane (2x the 32-byte runs of 16-column
+              // slabs; complex column bits 0..1 in-lane, 2..3 = lane & 3).
+              // Short-K steps -15-20%.  Single-chunk (kDirect) tiles only: next
+              // to the 128 promoted floats of the multi-chunk path ptxas spills
+              // ~0.5 KB per thread, so those keep the 16-column slabs.
+              const uint32_t stg_row = smem_u32(stg) + lane * 128;  // this lane's staged row
+              const uint32_t stg_rd = smem_u32(stg) + (lane >> 2) * 128;
+              const int sw = (lane >> 2) & 7;  // r & 7 of every row this lane reads
+#pragma unroll
+              for (int c0 = 0; c0 < HALF; c0 += 32) {
+#pragma unroll
+                for (int h16 = 0; h16 < 2; ++h16) {
+                  float a16[16];
+                  if constexpr (kDirect) {
+                    tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0 + 16 * h16), a16);
+                  } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) a16[i] = acc[c0 + 16 * h16 + i];
+                  }
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    float4 v =
+                        make_float4(a16[4 * i] * f1, a16[4 * i + 1] * f1, a16[4 * i + 2] * f1, a16[4 * i + 3] * f1);
+                    if (u2 != 0) { v.x *= f2; v.y *= f2; v.z *= f2; v.w *= f2; }
+                    local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg_row + (((4 * h16 + i) ^ (lane & 7)) << 4)),
+                                 "f"(a16[4 * i] * fy), "f"(a16[4 * i + 1] * fy), "f"(a16[4 * i + 2] * fy),
+                                 "f"(a16[4 * i + 3] * fy)
+                                 : "memory");
+                  }
+                }
+                __syncwarp();
+                const int g = lane & 3;
+                const long long jg = (g & 1) * 4 + ((g >> 1) ? col_bit(3) : 0ll) + ((c0 >> 5) & 1 ? col_bit(4) : 0ll) +
+                                     ((c0 >> 6) & 1 ? col_bit(5) : 0ll);
+#pragma unroll
+                for (int it = 0; it < 4; ++it) {
+                  const int r = it * 8 + (lane >> 2);
+                  float4 v0, v1;
+                  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                               : "=f"(v0.x), "=f"(v0.y), "=f"(v0.z), "=f"(v0.w)
+                               : "r"(stg_rd + it * 1024 + (((2 * g) ^ sw) << 4)));
+                  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                               : "=f"(v1.x), "=f"(v1.y), "=f"(v1.z), "=f"(v1.w)
+                               : "r"(stg_rd + it * 1024 + (((2 * g + 1) ^ sw) << 4)));
+                  const long long o = p.store_perm
+                                          ? (static_cast<long long>(row_tab[r]) << 3) + jg
+                                          : ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 8 * g) >> 1;
+                  const float x[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                  uint32_t hh[4], ll[4];
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const __half2 h = __floats2half2_rn(x[2 * j], x[2 * j + 1]);
+                    const float2 gg = __half22float2(h);
+                    hh[j] = h2_bits(h);
+                    ll[j] = h2_bits(__floats2half2_rn(x[2 * j] - gg.x, x[2 * j + 1] - gg.y));
+                  }
+                  if (p.stream_store) {
+                    __stcs(reinterpret_cast<uint4*>(c_bytes + 4 * o), make_uint4(hh[0], hh[1], hh[2], hh[3]));
+                    __stcs(reinterpret_cast<uint4*>(c_bytes + lo_plane + 4 * o), make_uint4(ll[0], ll[1], ll[2], ll[3]));
+                  } else {
+                    *reinterpret_cast<uint4*>(c_bytes + 4 * o) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+                    *reinterpret_cast<uint4*>(c_bytes + lo_plane + 4 * o) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+                  }
+                }
+                __syncwarp();
+              }
+              stored = true;
+            }
+          }
+          if (!stored) {
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += 16) {
             float a16[16];
@@ -1199,7 +1280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               float4 v = make_float4(a16[4 * i] * f1, a16[4 * i + 1] * f1, a16[4 * i + 2] * f1, a16[4 * i + 3] * f1);
               if (u2 != 0) { v.x *= f2; v.y *= f2; v.z *= f2; v.w *= f2; }
               local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
-              if (p.c_split)
+              if ((HALF < 32 || !kDirect) && p.c_split)
                 v = make_float4(a16[4 * i] * fy, a16[4 * i + 1] * fy, a16[4 * i + 2] * fy, a16[4 * i + 3] * fy);
               *reinterpret_cast<float4*>(stg + lane * Cfg::EPI_PITCH + 4 * i) = v;
             }
@@ -1207,7 +1288,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // column bits 3..5 of this 8-complex run (c0 < HALF <= 128: jhi < 64)
             const long long jc =
                 ((c0 >> 4) & 1 ? col_bit(3) : 0ll) + ((c0 >> 5) & 1 ? col_bit(4) : 0ll) + ((c0 >> 6) & 1 ? col_bit(5) : 0ll);
-            if (p.c_split) {
+            if ((HALF < 32 || !kDirect) && p.c_split) {
               // Split output, 4 complex per lane: one 16-byte hi and one
               // 16-byte lo store (half the store instructions of 2 complex).
 #pragma unroll
@@ -1217,7 +1298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const float4 v1 = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 8 * hf + 4);
                 long long o;  // complex offset of v0.xy (col bits 0..2 are the output's bits 0..2)
                 if (p.store_perm) {
-                  o = row_tab[r] + jc + 4 * hf;
+                  o = (static_cast<long long>(row_tab[r]) << 3) + jc + 4 * hf;
                 } else {
                   o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 8 * hf) >> 1;
                 }
@@ -1247,7 +1328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const float4 v = *reinterpret_cast<const float4*>(stg + r * Cfg::EPI_PITCH + 4 * c4);
               long long o;  // complex offset of v.xy in C
               if (p.store_perm) {
-                o = row_tab[r] + jc + lane_col_off;
+                o = (static_cast<long long>(row_tab[r]) << 3) + jc + lane_col_off;
               } else {
                 o = ((base - p.c) + static_cast<long long>(r) * p.n2 + c0 + 4 * c4) >> 1;
               }
@@ -1255,6 +1336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               else *reinterpret_cast<float4*>(p.c + 2 * o) = v;
             }
             __syncwarp();
+          }
           }
           if constexpr (kDirect) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
