@@ -392,8 +392,8 @@ def run_ours(args):
     # x1 draws, src/sampler.cpp:70-82) are made before the timed region
     host_nodes = torch.empty(info.node_bytes // 8, dtype=torch.complex64, pin_memory=True)
     eng.fold_nodes(text, out=host_nodes)
-    host_x1 = [[Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)]
-               for i in range(args.steps)]
+    host_x1 = [np.asarray([Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)],
+                          dtype=np.int32) for i in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()

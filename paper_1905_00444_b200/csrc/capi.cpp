@@ -655,20 +655,11 @@ int qsg_reassociate_plan(const char* circuit_text, int kind, const char* plan_te
 int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
                           const int64_t* slice_ids, int64_t k, double* amps_host, char* bitstrings_host) {
   return guarded([&] {
-    std::vector<std::vector<int>> xs;
-    for (int t = 0; t < nx1; ++t)
-      xs.emplace_back(x1_list + static_cast<std::size_t>(t) * n, x1_list + static_cast<std::size_t>(t + 1) * n);
-    const auto res = qsg::amplitude_batches(*e->impl, std::vector<int>(base_open, base_open + nbase), xs,
-                                            std::vector<std::int64_t>(slice_ids, slice_ids + k),
-                                            bitstrings_host != nullptr);
-    std::size_t o = 0;
-    for (const auto& draw : res)
-      for (const auto& [bits, amp] : draw) {
-        amps_host[2 * o] = amp.real();
-        amps_host[2 * o + 1] = amp.imag();
-        if (bitstrings_host) std::memcpy(bitstrings_host + o * static_cast<std::size_t>(n), bits.data(), static_cast<std::size_t>(n));
-        ++o;
-      }
+    if (n != e->impl->circuit().num_qubits()) throw std::invalid_argument("fold: bitstring length != qubit count");
+    if (nx1 < 0) throw std::invalid_argument("amplitude_batches: negative draw count");
+    qsg::amplitude_batches_into(*e->impl, std::vector<int>(base_open, base_open + nbase), x1_list,
+                                static_cast<std::size_t>(nx1), std::vector<std::int64_t>(slice_ids, slice_ids + k),
+                                amps_host, bitstrings_host);
   });
 }
 

@@ -1542,8 +1542,9 @@ long long resident_pairs(Kern kernel, int smem) {
 
 // The CTA-pair kernel covers 256 x 256 (real) tiles; QSG_TC_2SM=0 disables it.
 int pair_bn(std::int64_t n) {
+  static const int cap = env_int("QSG_TC_PAIR_BN_MAX", 256);  // A/B knob
   for (int bn : {256, 128, 64, 32})
-    if ((2 * n) % bn == 0) return bn;
+    if (bn <= cap && (2 * n) % bn == 0) return bn;
   return 0;
 }
 

@@ -1007,9 +1007,8 @@ ContractionPlan widen_plan(const Circuit& c, const ContractionPlan& plan, const 
   return p;
 }
 
-std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
-    Engine& wide, const std::vector<int>& base_open, const std::vector<std::vector<int>>& x1_list,
-    const std::vector<std::int64_t>& slice_ids, bool with_bitstrings) {
+void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                            const std::vector<std::int64_t>& slice_ids, double* amps_out, char* bits_out) {
   const int n = wide.circuit().num_qubits();
   const auto& wopen = wide.plan().open_qubits;
   std::vector<char> is_open(static_cast<std::size_t>(n), 0), is_base(static_cast<std::size_t>(n), 0);
@@ -1021,17 +1020,16 @@ std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
       throw std::invalid_argument("amplitude_batches: base open qubits must be open in the widened plan");
     is_base[static_cast<std::size_t>(q)] = 1;
   }
-  if (x1_list.empty()) return {};
+  if (nx1 == 0) return;
+  auto draw = [&](std::size_t t) { return x1_list + t * static_cast<std::size_t>(n); };
   // One contraction: the widened plan's closed qubits must agree across the list.
   std::vector<int> x1w(static_cast<std::size_t>(n), -1);
-  for (int q = 0; q < n; ++q) {
-    if (is_open[static_cast<std::size_t>(q)]) continue;
-    x1w[static_cast<std::size_t>(q)] = x1_list[0][static_cast<std::size_t>(q)];
-  }
-  for (const auto& x1 : x1_list) {
-    if (static_cast<int>(x1.size()) != n) throw std::invalid_argument("fold: bitstring length != qubit count");
+  for (int q = 0; q < n; ++q)
+    if (!is_open[static_cast<std::size_t>(q)]) x1w[static_cast<std::size_t>(q)] = draw(0)[q];
+  for (std::size_t t = 0; t < nx1; ++t) {
+    const int* x1 = draw(t);
     for (int q = 0; q < n; ++q) {
-      const int b = x1[static_cast<std::size_t>(q)];
+      const int b = x1[q];
       if ((b < 0) != static_cast<bool>(is_base[static_cast<std::size_t>(q)]))
         throw std::invalid_argument("x1 open qubits do not match the plan's open qubits");
       if (b > 1) throw std::invalid_argument("fold: output bits must be 0, 1 or -1 (open)");
@@ -1044,30 +1042,72 @@ std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
   std::vector<cdouble> amps;
   wide.results(&amps, nullptr);
   // Batch index of a full bitstring: bit (|open|-1-r) <-> r-th smallest open qubit (src/sampler.cpp:41-52).
-  const std::size_t nw = wopen.size(), nb = base_open.size();
-  std::vector<std::vector<std::pair<std::string, cdouble>>> out(x1_list.size());
-  for (std::size_t t = 0; t < x1_list.size(); ++t) {
-    auto& dst = out[t];
-    dst.reserve(std::size_t{1} << nb);
-    // wide index = fixed part (this draw's bits on the extra open qubits) +
-    // the base batch index's bits scattered to the base qubits' positions
+  // wide index = fixed part (this draw's bits on the extra open qubits) + the
+  // base batch index's bits scattered to the base qubits' positions.
+  const std::size_t nw = wopen.size(), nb = base_open.size(), per = std::size_t{1} << nb;
+  std::vector<std::size_t> base_pos(nb), extra_bit;
+  std::vector<int> extra_q;
+  for (std::size_t r = 0; r < nw; ++r) {
+    const int q = wopen[r];
+    const std::size_t bit = std::size_t{1} << (nw - 1 - r);
+    const auto it = std::find(base_open.begin(), base_open.end(), q);
+    if (it == base_open.end()) {
+      extra_q.push_back(q);
+      extra_bit.push_back(bit);
+    } else {
+      base_pos[static_cast<std::size_t>(it - base_open.begin())] = bit;  // base r-th smallest <-> batch bit nb-1-r
+    }
+  }
+  std::vector<std::size_t> scatter(per);  // wide-index part of each base batch index
+  for (std::size_t j = 0; j < per; ++j) {
+    std::size_t idx = 0;
+    for (std::size_t r = 0; r < nb; ++r)
+      if ((j >> (nb - 1 - r)) & 1) idx |= base_pos[r];
+    scatter[j] = idx;
+  }
+  for (std::size_t t = 0; t < nx1; ++t) {
     std::size_t fixed = 0;
-    std::vector<std::size_t> base_pos(nb);
-    for (std::size_t r = 0; r < nw; ++r) {
-      const int q = wopen[r];
-      const std::size_t bit = std::size_t{1} << (nw - 1 - r);
-      const auto it = std::find(base_open.begin(), base_open.end(), q);
-      if (it == base_open.end()) {
-        if (x1_list[t][static_cast<std::size_t>(q)] == 1) fixed |= bit;
-      } else {
-        base_pos[static_cast<std::size_t>(it - base_open.begin())] = bit;  // base r-th smallest <-> batch bit nb-1-r
+    for (std::size_t e = 0; e < extra_q.size(); ++e)
+      if (draw(t)[extra_q[e]] == 1) fixed |= extra_bit[e];
+    double* out = amps_out + 2 * t * per;
+    for (std::size_t j = 0; j < per; ++j) {
+      const cdouble a = amps[fixed | scatter[j]];
+      out[2 * j] = a.real();
+      out[2 * j + 1] = a.imag();
+    }
+    if (bits_out) {
+      const std::vector<int> x1(draw(t), draw(t) + n);
+      for (std::size_t j = 0; j < per; ++j) {
+        const std::string b = merge_bits(x1, base_open, j);
+        std::memcpy(bits_out + (t * per + j) * static_cast<std::size_t>(n), b.data(), static_cast<std::size_t>(n));
       }
     }
-    for (std::size_t j = 0; j < (std::size_t{1} << nb); ++j) {
-      std::size_t idx = fixed;
-      for (std::size_t r = 0; r < nb; ++r)
-        if ((j >> (nb - 1 - r)) & 1) idx |= base_pos[r];
-      dst.emplace_back(with_bitstrings ? merge_bits(x1_list[t], base_open, j) : std::string(), amps[idx]);
+  }
+}
+
+std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
+    Engine& wide, const std::vector<int>& base_open, const std::vector<std::vector<int>>& x1_list,
+    const std::vector<std::int64_t>& slice_ids, bool with_bitstrings) {
+  const int n = wide.circuit().num_qubits();
+  std::vector<int> flat;
+  flat.reserve(x1_list.size() * static_cast<std::size_t>(n));
+  for (const auto& x1 : x1_list) {
+    if (static_cast<int>(x1.size()) != n) throw std::invalid_argument("fold: bitstring length != qubit count");
+    flat.insert(flat.end(), x1.begin(), x1.end());
+  }
+  const std::size_t per = std::size_t{1} << base_open.size();
+  std::vector<double> amps(2 * per * x1_list.size());
+  std::vector<char> bits(with_bitstrings ? per * x1_list.size() * static_cast<std::size_t>(n) : 0);
+  amplitude_batches_into(wide, base_open, flat.data(), x1_list.size(), slice_ids, amps.data(),
+                         with_bitstrings ? bits.data() : nullptr);
+  std::vector<std::vector<std::pair<std::string, cdouble>>> out(x1_list.size());
+  for (std::size_t t = 0; t < x1_list.size(); ++t) {
+    out[t].reserve(per);
+    for (std::size_t j = 0; j < per; ++j) {
+      const std::size_t o = t * per + j;
+      out[t].emplace_back(with_bitstrings ? std::string(bits.data() + o * static_cast<std::size_t>(n), static_cast<std::size_t>(n))
+                                          : std::string(),
+                          cdouble(amps[2 * o], amps[2 * o + 1]));
     }
   }
   return out;

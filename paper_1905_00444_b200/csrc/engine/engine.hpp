@@ -238,5 +238,9 @@ ContractionPlan widen_plan(const Circuit& c, const ContractionPlan& plan, const 
 std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
     Engine& wide, const std::vector<int>& base_open, const std::vector<std::vector<int>>& x1_list,
     const std::vector<std::int64_t>& slice_ids, bool with_bitstrings = true);
+// Same, flat buffers: x1_list nx1 x n ints; writes nx1 x 2^|base| (re, im)
+// and, if bits_out, the bitstrings (n chars each) in the same order.
+void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                            const std::vector<std::int64_t>& slice_ids, double* amps_out, char* bits_out);
 
 }  // namespace qsg
