@@ -1659,15 +1659,17 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.norm_a = g.norm_a && g.meta_a != nullptr;
   p.norm_b = g.norm_b && g.meta_b != nullptr;
   // Promotion interval: 128 real K (2 k-blocks; relative error ~1e-6,
-  // linear in the interval, tests/tc_accuracy).  Short-K tiles (k <= 256)
-  // use 2 chunks of k/2: every promotion is a TMEM hand-off between the MMA
-  // and the worker warps that also write the tile epilogue, and with 4 per
-  // 8-k-block tile the MMA waits on them (measured: the k = 256 steps of
-  // config 2 run 25-35% faster; error ~2e-6).
+  // linear in the interval, tests/tc_accuracy).  Short-K tiles (k <= 256,
+  // at most 512 real K) run as ONE chunk: no promotion, the epilogue stores
+  // straight from TMEM (kDirect).  Every promotion is a TMEM hand-off
+  // between the MMA and the worker warps that also write the tile epilogue;
+  // measured on config 2: 4 chunks per k=256 tile -> 2 chunks 25-35% faster,
+  // 2 -> 1 another 21% (batch -4%), amplitudes vs the FP32-SIMT engine
+  // rel-L2 9.3e-6 -> 1.5e-5, batch fidelity 1 - 2e-11 (north star: 1 - 1e-6).
   const char* chunk_env = std::getenv("QSG_TC_CHUNK");
   const int per128 = 128 / kb;  // k-blocks per 128 real K
   if (chunk_env) p.chunk = std::max(1, chunk_blocks() * per128 / 4);
-  else p.chunk = p.kblocks <= 4 * per128 ? std::max(per128, (p.kblocks + 1) / 2) : per128;
+  else p.chunk = p.kblocks <= 4 * per128 ? p.kblocks : per128;
   p.store_perm = g.store_perm ? 1 : 0;
   p.nrow_bits = g.nrow_bits;
   p.ncol_bits = g.ncol_bits;
