@@ -176,6 +176,7 @@ Engine::~Engine() {
   if (metas_) cudaFree(metas_);
   if (acc_) cudaFree(acc_);
   if (per_slice_) cudaFree(per_slice_);
+  if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -862,9 +863,18 @@ void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off,
   launches_ += launches;
 }
 
+std::vector<std::int64_t> Engine::run_key(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) const {
+  std::vector<std::int64_t> key(slice_ids);
+  key.push_back(-1);
+  key.insert(key.end(), node_x1_off_.begin(), node_x1_off_.end());
+  key.push_back(reset ? 1 : 0);
+  key.push_back(per_slice ? 1 : 0);
+  key.push_back(reinterpret_cast<std::int64_t>(per_slice_));
+  return key;
+}
+
 void Engine::run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) {
   check(cudaSetDevice(opt_.device), "cudaSetDevice");
-  if (reset) check(cudaMemsetAsync(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_), stream_), "acc reset");
   if (per_slice) {
     const std::int64_t need = static_cast<std::int64_t>(slice_ids.size()) * batch_;
     if (need > per_slice_cap_) {
@@ -878,6 +888,61 @@ void Engine::run(const std::vector<std::int64_t>& slice_ids, bool reset, bool pe
     per_slice_used_ = 0;
   }
   if (events_pending_) profile();  // fold finished timings before reusing events
+  static const bool env_off = std::getenv("QSG_GRAPH") && std::getenv("QSG_GRAPH")[0] == '0';
+  const bool graphable = opt_.graphs && graphs_ok_ && !env_off && !opt_.profile && host_arena_bytes_ == 0;
+  if (!graphable) {
+    enqueue_run(slice_ids, reset, per_slice);
+    return;
+  }
+  auto key = run_key(slice_ids, reset, per_slice);
+  if (graph_exec_ && key == graph_key_) {
+    check(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
+    launches_ += graph_launches_;
+    return;
+  }
+  if (key != last_key_) {  // first occurrence: eager (also the first-use setup of every kernel)
+    last_key_ = std::move(key);
+    enqueue_run(slice_ids, reset, per_slice);
+    return;
+  }
+  // Second identical run in a row: capture it once, replay from now on.
+  if (graph_exec_) {
+    cudaGraphExecDestroy(graph_exec_);
+    graph_exec_ = nullptr;
+  }
+  const std::int64_t before = launches_;
+  cudaGraph_t graph = nullptr;
+  check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "graph capture");
+  try {
+    enqueue_run(slice_ids, reset, per_slice);
+  } catch (...) {
+    cudaStreamEndCapture(stream_, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    graphs_ok_ = false;
+    launches_ = before;
+    cudaGetLastError();
+    enqueue_run(slice_ids, reset, per_slice);
+    return;
+  }
+  const cudaError_t ce = cudaStreamEndCapture(stream_, &graph);
+  cudaError_t ie = ce;
+  if (ce == cudaSuccess) ie = cudaGraphInstantiate(&graph_exec_, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) {  // capture unsupported here: stay eager
+    graph_exec_ = nullptr;
+    graphs_ok_ = false;
+    launches_ = before;
+    cudaGetLastError();
+    enqueue_run(slice_ids, reset, per_slice);
+    return;
+  }
+  graph_launches_ = launches_ - before;
+  graph_key_ = last_key_;
+  check(cudaGraphLaunch(graph_exec_, stream_), "graph launch");
+}
+
+void Engine::enqueue_run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) {
+  if (reset) check(cudaMemsetAsync(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_), stream_), "acc reset");
   for (std::size_t s = 0; s < slice_ids.size(); ++s) {
     const auto digits = cut_digits(shape_, plan_.cut, slice_ids[s]);
     std::vector<std::int64_t> node_off(node_x1_off_);

@@ -50,6 +50,12 @@ struct EngineOptions {
   std::int64_t memory_budget = 0;
   int pipeline_depth = 2;
   std::int64_t device_memory = 0;
+  // Replay a run identical to the previous one (same slices, x1 views and
+  // flags) as a CUDA graph captured on its second occurrence: the
+  // launch-bound small configurations (config 1: ~140 kernels in 0.5 ms)
+  // stop paying one host launch per kernel.  Off while profiling and for
+  // out-of-core programs; QSG_GRAPH=0 disables.
+  bool graphs = true;
 };
 
 struct OpProfile {
@@ -208,6 +214,13 @@ class Engine {
   std::int64_t per_slice_cap_ = 0;
   std::int64_t per_slice_used_ = 0;
   std::int64_t launches_ = 0;
+  // CUDA graph of the last repeated run (see EngineOptions::graphs).
+  void enqueue_run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice);
+  std::vector<std::int64_t> run_key(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) const;
+  std::vector<std::int64_t> last_key_, graph_key_;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  std::int64_t graph_launches_ = 0;
+  bool graphs_ok_ = true;
 
   std::vector<cudaEvent_t> ev_;
   std::vector<double> op_ms_;

@@ -393,3 +393,27 @@ def test_reassociated_plan_same_amplitudes(gpu, tc, monkeypatch):
     sv = O.evolve(text)
     exact = np.array([sv[int(b, 2)] for b in bits])
     assert rel(got, exact) < 1e-4
+
+
+def test_repeated_runs_replay_as_graph(gpu, cases, monkeypatch):
+    """A run repeated with the same slices and x1 is captured once and replayed
+    as a CUDA graph: bit-identical results, same kernel count per run, and a
+    new x1 / slice list falls back to eager launches."""
+    _, meta = cases
+    case = next(c for c in meta["cases"] if c["slices"] >= 2)
+    text = gpu.generate_rqc(case["rows"], case["cols"], case["m"], case["seed"])
+    monkeypatch.setenv("QSG_TC_MIN_FLOPS", "0")
+    out, counts = [], []
+    with gpu.Engine(text, case["plan"]) as e:
+        e.prepare(case["x1"])
+        for _ in range(4):
+            n0 = e.launches()
+            e.run(range(case["slices"]), reset=True, per_slice=True)
+            out.append(e.results())
+            counts.append(e.launches() - n0)
+        e.run([0], reset=True)
+        single = e.results()
+    assert len(set(counts)) == 1 and counts[0] > 0
+    for amps, per in out[1:]:
+        assert np.array_equal(amps, out[0][0]) and np.array_equal(per, out[0][1])
+    assert rel(single, out[0][1][0]) < 1e-12
