@@ -440,14 +440,20 @@ def run_ours(args):
     elif top["tensor_cores"]:
         bound, peak_val, peak_note = "tensor", peaks["bf16_tflops"] / 2.0 / 3.0, (
             f"3xTF32 ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 2 (tf32) / 3 (passes)")
+    elif top["bytes"] > 0 and top["flops"] / top["bytes"] < fp32_peak * 1e12 / (peaks["hbm_gbs"] * 1e9):
+        # below the FP32 ridge (11.4 flop/B): the SIMT step is HBM-bound
+        bound, peak_val, peak_note = "hbm", peaks["hbm_gbs"], f"{peak_src} HBM copy bandwidth (GB/s)"
+        achieved = top["bytes"] / (top_ms / 1e3) / 1e9
     else:
         bound, peak_val, peak_note = "tensor", fp32_peak, (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x "
                                                            f"{smx:.0f} MHz ({peak_src} sm_max_mhz)")
-    kernel_name = (f"cgemm_tc ({split})" if top["tensor_cores"] else "cgemm_simt") + \
+    simt_name = "cgemm_narrow" if top["n"] <= 32 and top["m"] >= 1024 else "cgemm_simt"
+    kernel_name = (f"cgemm_tc ({split})" if top["tensor_cores"] else simt_name) + \
         f" step s{top['step']:03d} m={top['m']} n={top['n']} k={top['k']}"
     perm_ms = sum(p["ms_total"] for p in perms)
     perm_bytes = sum(p["bytes"] * p["executions"] for p in perms)
-    roof = {"bound": bound, "achieved": achieved, "peak": peak_val, "unit": "TFLOP/s", "frac": achieved / peak_val,
+    roof = {"bound": bound, "achieved": achieved, "peak": peak_val, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+            "frac": achieved / peak_val,
             "traffic": None, "kernel": kernel_name,
             "kernel_share_of_step": top["ms_total"] / total_ms, "peak_source": peak_note,
             "fp32_simt_peak_tflops": fp32_peak,

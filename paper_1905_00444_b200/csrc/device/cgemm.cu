@@ -214,9 +214,9 @@ __global__ void __launch_bounds__(NT) splitk_reduce_kernel(const KParams p, int 
 // shared memory with coalesced loads (T layout: along m; N layout: along k),
 // B's chunk (<= 32 x 16) is broadcast from shared memory, and each thread
 // stores its contiguous row.  HBM-bound: 8 (m k + m n) bytes per launch.
-constexpr int NR = 128, NKC = 32, NNW = 16;
+constexpr int NR = 128, NKC = 32;
 
-template <bool TA, bool TB>
+template <bool TA, bool TB, int NNW>
 __global__ void __launch_bounds__(NR) cgemm_narrow_kernel(const KParams p) {
   __shared__ float2 As[NKC][NR + 1];
   __shared__ float2 Bs[NKC][NNW];
@@ -277,7 +277,19 @@ __global__ void __launch_bounds__(NR) cgemm_narrow_kernel(const KParams p) {
   }
 }
 
-bool use_narrow(std::int64_t m, std::int64_t n) { return n <= NNW && m >= 1024; }
+bool use_narrow(std::int64_t m, std::int64_t n) { return n <= 32 && m >= 1024; }
+
+template <int NNW>
+void launch_narrow(const GemmArgs& g, const KParams& p, cudaStream_t stream) {
+  const dim3 grid(static_cast<unsigned>((g.m + NR - 1) / NR));
+  if (g.trans_a) {
+    if (g.trans_b) cgemm_narrow_kernel<true, true, NNW><<<grid, NR, 0, stream>>>(p);
+    else cgemm_narrow_kernel<true, false, NNW><<<grid, NR, 0, stream>>>(p);
+  } else {
+    if (g.trans_b) cgemm_narrow_kernel<false, true, NNW><<<grid, NR, 0, stream>>>(p);
+    else cgemm_narrow_kernel<false, false, NNW><<<grid, NR, 0, stream>>>(p);
+  }
+}
 
 int sm_count() {
   static int n = [] {
@@ -299,6 +311,8 @@ int choose_splits(std::int64_t m, std::int64_t n, std::int64_t k) {
 }
 
 }  // namespace
+
+bool cgemm_narrow(std::int64_t m, std::int64_t n) { return use_narrow(m, n); }
 
 std::int64_t cgemm_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   if (use_narrow(m, n)) return 0;
@@ -324,14 +338,8 @@ cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches) {
   if (use_narrow(g.m, g.n) && g.k > 0) {
     const std::int64_t blocks = (g.m + NR - 1) / NR;
     if (blocks > 0x7fffffff) throw std::length_error("cgemm: m too large for the grid");
-    const dim3 grid(static_cast<unsigned>(blocks));
-    if (g.trans_a) {
-      if (g.trans_b) cgemm_narrow_kernel<true, true><<<grid, NR, 0, stream>>>(p);
-      else cgemm_narrow_kernel<true, false><<<grid, NR, 0, stream>>>(p);
-    } else {
-      if (g.trans_b) cgemm_narrow_kernel<false, true><<<grid, NR, 0, stream>>>(p);
-      else cgemm_narrow_kernel<false, false><<<grid, NR, 0, stream>>>(p);
-    }
+    if (g.n <= 16) launch_narrow<16>(g, p, stream);
+    else launch_narrow<32>(g, p, stream);
     if (launches) ++*launches;
     return cudaGetLastError();
   }

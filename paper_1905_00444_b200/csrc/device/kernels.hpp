@@ -73,6 +73,9 @@ struct GemmArgs {
   bool a_presplit = false;
 };
 std::int64_t cgemm_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
+// True when cgemm runs the narrow-N kernel (n <= 32, m >= 1024): one thread
+// per output row, HBM-bound (8 (m k + m n + k n) bytes).
+bool cgemm_narrow(std::int64_t m, std::int64_t n);
 cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
 
 // ---- K3: accumulate --------------------------------------------------------

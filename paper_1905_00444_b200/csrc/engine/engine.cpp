@@ -324,7 +324,17 @@ void Engine::compile() {
               dev::cgemm_tc_workspace_bytes(mm, nn2, k, ta, tb) <= kMaxTcWorkspace;
       const double bytes = (ch.use_a ? 0.0 : 16.0 * X.volume()) + (ch.use_b ? 0.0 : 16.0 * Y.volume()) +
                            (ch.tc ? dev::cgemm_tc_prep_bytes(mm, nn2, k) : 0.0);
-      ch.cost = bytes / kHbm + flops / (ch.tc ? dev::cgemm_tc_rate(mm, nn2, k) : kSimtRate);
+      double gemm_s;
+      if (ch.tc) {
+        gemm_s = flops / dev::cgemm_tc_rate(mm, nn2, k);
+      } else if (dev::cgemm_narrow(mm, nn2)) {  // HBM-bound narrow-N kernel
+        gemm_s = 8.0 * static_cast<double>(mm * k + mm * nn2 + k * nn2) / kHbm;
+      } else {  // 64 x 128 tiles: padded rows / columns are computed too
+        const double pad = static_cast<double>((mm + 63) / 64 * 64) / static_cast<double>(mm) *
+                           static_cast<double>((nn2 + 127) / 128 * 128) / static_cast<double>(nn2);
+        gemm_s = flops * pad / kSimtRate;
+      }
+      ch.cost = bytes / kHbm + gemm_s;
       return ch;
     };
     Choice best = evaluate(false, con_l, false);

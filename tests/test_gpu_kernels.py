@@ -120,7 +120,8 @@ def test_normalize_inplace(gpu):
                                          (1 << 14, 256, 256, 0, 0),
                                          # narrow-N kernel (n <= 16, m >= 1024): T / N layouts, ragged k and n
                                          (1 << 20, 16, 16, 1, 0), (5000, 16, 16, 0, 0), (4099, 7, 40, 0, 1),
-                                         (3000, 16, 33, 1, 1), (2048, 1, 256, 0, 0), (1024, 16, 1, 1, 0)])
+                                         (3000, 16, 33, 1, 1), (2048, 1, 256, 0, 0), (1024, 16, 1, 1, 0),
+                                         (1 << 17, 32, 16, 1, 1), (5000, 29, 70, 0, 0), (1100, 17, 8, 1, 0)])
 def test_cgemm_device_shapes_vs_fp64(gpu, m, n, k, ta, tb):
     import torch
     g = torch.Generator().manual_seed(m * 7 + n * 3 + k)
