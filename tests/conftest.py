@@ -35,3 +35,19 @@ def gpu():
         pytest.fail("GPU test selected but no CUDA device is visible")
     import paper_1905_00444_b200 as Q
     return Q
+
+
+def sweep_plan(Q, rows, cols, m, seed, nopen):
+    """Column-major sweep chained onto one accumulator (the config 3/4 plan
+    shape) on a small grid, with the first `nopen` qubits of the last row open:
+    (circuit text, plan JSON, open qubits)."""
+    import json
+    text = Q.generate_rqc(rows, cols, m, seed)
+    nodes = [r * cols + c for c in range(cols) for r in range(rows)]
+    order, acc = [], f"n_{nodes[0]:03d}"
+    for i, q in enumerate(nodes[1:]):
+        order.append([acc, f"n_{q:03d}"])
+        acc = f"s{i:03d}"
+    opn = sorted((rows - 1) * cols + c for c in range(nopen))
+    draft = {"version": 1, "open_qubits": opn, "cut": {"labels": [], "group": 1}, "order": order}
+    return text, Q.plan_json(text, opn, Q.PLAN_JSON, json.dumps(draft)), opn

@@ -15,7 +15,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, ROOT
+from conftest import GOLDEN, ROOT, sweep_plan
 
 pytestmark = pytest.mark.gpu
 
@@ -377,10 +377,9 @@ def test_reassociated_plan_same_amplitudes(gpu, tc, monkeypatch):
     """A sweep plan and its reassociated tree give the same batch (1e-5) and
     both match the double state vector (1e-4)."""
     import qsim_oracle as O
-    from test_program import _sweep_plan
     if tc:
         monkeypatch.setenv("QSG_TC_MIN_FLOPS", "0")
-    text, plan, opn = _sweep_plan(4, 5, 16, 3, 4)
+    text, plan, opn = sweep_plan(gpu, 4, 5, 16, 3, 4)
     new, k = gpu.reassociate_plan(text, plan)
     assert k > 0
     x1 = [-1 if q in opn else (q * 5 + 1) % 2 for q in range(20)]

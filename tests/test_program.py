@@ -6,7 +6,7 @@ import os
 import pytest
 
 import paper_1905_00444_b200 as Q
-from conftest import ROOT
+from conftest import ROOT, sweep_plan
 
 HBM_BYTES = 180e9
 
@@ -69,23 +69,10 @@ def test_out_of_core_automatic_budget():
         assert arena + 2 * slot <= 0.92 * dev
 
 
-def _sweep_plan(rows, cols, m, seed, nopen):
-    """Column-major sweep chained onto one accumulator (the config 3/4 plan shape)."""
-    text = Q.generate_rqc(rows, cols, m, seed)
-    nodes = [r * cols + c for c in range(cols) for r in range(rows)]
-    order, acc = [], f"n_{nodes[0]:03d}"
-    for i, q in enumerate(nodes[1:]):
-        order.append([acc, f"n_{q:03d}"])
-        acc = f"s{i:03d}"
-    opn = sorted((rows - 1) * cols + c for c in range(nopen))
-    draft = {"version": 1, "open_qubits": opn, "cut": {"labels": [], "group": 1}, "order": order}
-    return text, Q.plan_json(text, opn, Q.PLAN_JSON, json.dumps(draft)), opn
-
-
 def test_reassociate_plan_sweeps():
     """The opt-in tree rewrite keeps cut, slices, open qubits and peak bounds,
     lowers the Eq.(1) flops of sweep plans, and is idempotent."""
-    text, plan, _ = _sweep_plan(4, 5, 16, 3, 4)
+    text, plan, _ = sweep_plan(Q, 4, 5, 16, 3, 4)
     new, k = Q.reassociate_plan(text, plan)
     a, b = json.loads(plan), json.loads(new)
     assert k > 0 and len(b["order"]) == len(a["order"])
