@@ -218,7 +218,7 @@ constexpr int NR = 128, NKC = 32;
 
 template <bool TA, bool TB, int NNW>
 __global__ void __launch_bounds__(NR) cgemm_narrow_kernel(const KParams p) {
-  __shared__ float2 As[NKC][NR + 1];
+  __shared__ __align__(16) float2 As[NKC][NR + 1];
   __shared__ float2 Bs[NKC][NNW];
   const int tid = threadIdx.x;
   const long long m0 = static_cast<long long>(blockIdx.x) * NR;
@@ -252,7 +252,28 @@ __global__ void __launch_bounds__(NR) cgemm_narrow_kernel(const KParams p) {
   const int shift = sa + sb;
   float local = 0.f;
   const long long gm = m0 + tid;
-  if (gm < M) {
+  if (N == NNW && m0 + NR <= M) {
+    // Full block: its 128 rows x NNW columns are one contiguous run of C.
+    // Stage them through the (now idle) A buffer -- 16-byte chunk c of row
+    // r at slot c ^ (r mod NNW/2), conflict-free both ways -- and store the
+    // run with consecutive threads on consecutive 16-byte pieces.
+    constexpr int CH = NNW / 2;  // float4 chunks per row
+    float4* stage = reinterpret_cast<float4*>(&As[0][0]);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const float4 v = make_float4(scalbnf(acc[2 * c].x, -shift), scalbnf(acc[2 * c].y, -shift),
+                                   scalbnf(acc[2 * c + 1].x, -shift), scalbnf(acc[2 * c + 1].y, -shift));
+      local = fmaxf(local, fmaxf(v.x * v.x + v.y * v.y, v.z * v.z + v.w * v.w));
+      stage[tid * CH + (c ^ (tid & (CH - 1)))] = v;
+    }
+    __syncthreads();
+    float4* out = reinterpret_cast<float4*>(p.c + m0 * N);
+#pragma unroll 4
+    for (int l = tid; l < NR * CH; l += NR) {
+      const int r = l / CH, c = l % CH;
+      out[l] = stage[r * CH + (c ^ (r & (CH - 1)))];
+    }
+  } else if (gm < M) {
 #pragma unroll
     for (int j = 0; j < NNW; ++j) {
       const float2 v = make_float2(scalbnf(acc[j].x, -shift), scalbnf(acc[j].y, -shift));
