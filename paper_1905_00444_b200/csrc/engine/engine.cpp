@@ -175,6 +175,7 @@ Engine::~Engine() {
   if (store_stream_) cudaStreamDestroy(store_stream_);
   if (metas_) cudaFree(metas_);
   if (acc_) cudaFree(acc_);
+  if (acc_host_) cudaFreeHost(acc_host_);
   if (per_slice_) cudaFree(per_slice_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -981,10 +982,14 @@ void Engine::enqueue_run(const std::vector<std::int64_t>& slice_ids, bool reset,
 
 void Engine::results(std::vector<cdouble>* amps, std::vector<cdouble>* per_slice) {
   check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  const std::size_t acc_bytes = sizeof(double2) * static_cast<std::size_t>(batch_);
   if (amps) {
     amps->resize(static_cast<std::size_t>(batch_));
-    check(cudaMemcpyAsync(amps->data(), acc_, sizeof(double2) * static_cast<std::size_t>(batch_), cudaMemcpyDeviceToHost,
-                          stream_),
+    // Large batches (widened x1 plans: 2^16 amplitudes) go through a pinned
+    // staging buffer: a pageable D2H runs at a fraction of the link rate.
+    if (acc_bytes >= (64u << 10) && !acc_host_) check(cudaMallocHost(&acc_host_, acc_bytes), "pinned staging");
+    check(cudaMemcpyAsync(acc_host_ ? static_cast<void*>(acc_host_) : static_cast<void*>(amps->data()), acc_, acc_bytes,
+                          cudaMemcpyDeviceToHost, stream_),
           "result copy");
   }
   if (per_slice) {
@@ -995,6 +1000,7 @@ void Engine::results(std::vector<cdouble>* amps, std::vector<cdouble>* per_slice
             "per-slice copy");
   }
   check(cudaStreamSynchronize(stream_), "result sync");
+  if (amps && acc_host_) std::memcpy(amps->data(), acc_host_, acc_bytes);
 }
 
 void Engine::synchronize() {

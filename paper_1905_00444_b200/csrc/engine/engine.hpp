@@ -210,6 +210,7 @@ class Engine {
   dev::TMeta* metas_ = nullptr;
   int nmeta_ = 0;
   double2* acc_ = nullptr;
+  double2* acc_host_ = nullptr;  // pinned staging of the batch for results()
   double2* per_slice_ = nullptr;
   std::int64_t per_slice_cap_ = 0;
   std::int64_t per_slice_used_ = 0;
