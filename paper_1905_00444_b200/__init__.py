@@ -570,7 +570,7 @@ class Engine:
         nx1, n = xs.shape
         ids = np.ascontiguousarray(np.asarray(list(slice_ids), dtype=np.int64))
         per = 1 << len(b)
-        amps = np.zeros(2 * per * nx1, dtype=np.float64)
+        amps = np.empty(2 * per * nx1, dtype=np.float64)  # every entry is written
         bits = C.create_string_buffer(max(1, n * per * nx1)) if bitstrings else None
         _check(lib().qsg_amplitude_batches(self._h, pb, len(b), _p(xs, C.c_int), nx1, n, _p(ids, C.c_int64), len(ids),
                                            _p(amps, C.c_double), bits))

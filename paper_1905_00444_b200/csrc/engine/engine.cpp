@@ -1003,6 +1003,15 @@ void Engine::results(std::vector<cdouble>* amps, std::vector<cdouble>* per_slice
   if (amps && acc_host_) std::memcpy(amps->data(), acc_host_, acc_bytes);
 }
 
+const cdouble* Engine::results_pinned() {
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  const std::size_t acc_bytes = sizeof(double2) * static_cast<std::size_t>(batch_);
+  if (!acc_host_) check(cudaMallocHost(&acc_host_, acc_bytes), "pinned staging");
+  check(cudaMemcpyAsync(acc_host_, acc_, acc_bytes, cudaMemcpyDeviceToHost, stream_), "result copy");
+  check(cudaStreamSynchronize(stream_), "result sync");
+  return reinterpret_cast<const cdouble*>(acc_host_);
+}
+
 void Engine::synchronize() {
   check(cudaSetDevice(opt_.device), "cudaSetDevice");
   check(cudaStreamSynchronize(stream_), "sync");
@@ -1120,8 +1129,7 @@ void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, con
   }
   wide.prepare(x1w);
   wide.run(slice_ids, /*reset=*/true, /*per_slice=*/false);
-  std::vector<cdouble> amps;
-  wide.results(&amps, nullptr);
+  const cdouble* amps = wide.results_pinned();
   // Batch index of a full bitstring: bit (|open|-1-r) <-> r-th smallest open qubit (src/sampler.cpp:41-52).
   // wide index = fixed part (this draw's bits on the extra open qubits) + the
   // base batch index's bits scattered to the base qubits' positions.

@@ -109,6 +109,9 @@ class Engine {
 
   // Copies results to the host (synchronises the stream).
   void results(std::vector<cdouble>* amps, std::vector<cdouble>* per_slice);
+  // The batch in the engine's pinned staging buffer (synchronises; valid
+  // until the next results call): no allocation on the hot path.
+  const cdouble* results_pinned();
   void synchronize();
 
   std::int64_t launches() const { return launches_; }
