@@ -68,8 +68,8 @@ __global__ void __launch_bounds__(kThreads) permute_bits_kernel(const float2* __
   __syncthreads();
   const int tsize = 1 << p.tbits;
   const int lane = tid & 31;
-  for (long long t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-    // Tile base offsets: lane k contributes tile bit k (and k + 32).
+  // Tile base offsets: lane k contributes tile bit k (and k + 32).
+  auto bases = [&](long long t, long long& base_in, long long& base_out) {
     unsigned long long bin = 0, bout = 0;
     for (int k = lane; k < p.nrest; k += 32)
       if ((t >> k) & 1) {
@@ -80,26 +80,45 @@ __global__ void __launch_bounds__(kThreads) permute_bits_kernel(const float2* __
     const unsigned bin_hi = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(bin >> 32));
     const unsigned bout_lo = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(bout));
     const unsigned bout_hi = __reduce_or_sync(0xffffffffu, static_cast<unsigned>(bout >> 32));
-    const long long base_in = p.in_base + static_cast<long long>((static_cast<unsigned long long>(bin_hi) << 32) | bin_lo);
-    const long long base_out = static_cast<long long>((static_cast<unsigned long long>(bout_hi) << 32) | bout_lo);
-
-    float2 v[(1 << kTileBits) / kThreads];
+    base_in = p.in_base + static_cast<long long>((static_cast<unsigned long long>(bin_hi) << 32) | bin_lo);
+    base_out = static_cast<long long>((static_cast<unsigned long long>(bout_hi) << 32) | bout_lo);
+  };
+  constexpr int kPer = (1 << kTileBits) / kThreads;
+  float2 v[kPer];
+  auto load = [&](long long base_in) {
 #pragma unroll
-    for (int j = 0; j < (1 << kTileBits) / kThreads; ++j) {
+    for (int j = 0; j < kPer; ++j) {
       const int e = tid + j * kThreads;
       if (e < tsize) v[j] = __ldcs(in + base_in + s_in_lo[e & 31] + s_in_hi[e >> 5]);
     }
+  };
+  // Software pipeline: the next tile's loads are in flight while the current
+  // tile drains from shared memory to HBM.
+  long long t = blockIdx.x;
+  if (t >= p.ntiles) return;
+  long long base_in, base_out;
+  bases(t, base_in, base_out);
+  load(base_in);
+  while (true) {
 #pragma unroll
-    for (int j = 0; j < (1 << kTileBits) / kThreads; ++j) {
+    for (int j = 0; j < kPer; ++j) {
       const int e = tid + j * kThreads;
       if (e < tsize) tile[swz(s_f_lo[e & 31] | s_f_hi[e >> 5])] = v[j];
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < (1 << kTileBits) / kThreads; ++j) {
-      const int f = tid + j * kThreads;
-      if (f < tsize) __stcs(out + base_out + s_out_lo[f & 31] + s_out_hi[f >> 5], tile[swz(f)]);
+    const long long cur_out = base_out;
+    const long long tn = t + gridDim.x;
+    if (tn < p.ntiles) {
+      bases(tn, base_in, base_out);
+      load(base_in);
     }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int f = tid + j * kThreads;
+      if (f < tsize) __stcs(out + cur_out + s_out_lo[f & 31] + s_out_hi[f >> 5], tile[swz(f)]);
+    }
+    if (tn >= p.ntiles) break;
+    t = tn;
     __syncthreads();
   }
 }

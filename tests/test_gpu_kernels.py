@@ -33,7 +33,7 @@ def test_transpose_identity_involution_and_large_bit_permutations(gpu):
     assert np.array_equal(gpu.transpose(t, [0, 1, 2]), t)
     u = gpu.transpose(gpu.transpose(t, [2, 0, 1]), [1, 2, 0])
     assert np.array_equal(u, t)
-    for rank in (11, 17, 20, 23):
+    for rank in (7, 11, 17, 20, 23):
         x = (rng.random(2**rank) - 0.5 + 1j * (rng.random(2**rank) - 0.5)).astype(np.complex64).reshape([2] * rank)
         perm = list(rng.permutation(rank))
         assert np.array_equal(gpu.transpose(x, perm), np.transpose(x, perm))
