@@ -277,7 +277,7 @@ def run_reference_arm(args):
                                    f"(heavy flops / heavy rate + other flops / prefix rate)"},
         "e2e": {"value": amps, "unit": "amplitudes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -517,14 +517,27 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": None, "unit": "amplitudes/s", "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {exc}"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     eng.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
 
 
+_JSON_FD = 1
+
+
+def emit(line):
+    """The result line goes to the real stdout; everything else (NCCL's
+    version banner, library chatter) was redirected to stderr by main()."""
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
