@@ -87,3 +87,24 @@ def test_reassociate_plan_sweeps():
     assert b3["per_slice"]["flops"] < a3["per_slice"]["flops"]
     assert b3["per_slice"]["peak_memory"] <= a3["per_slice"]["peak_memory"]
     assert "gemm" in Q.program_listing(c3, n3)
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libqsim_ref.so")),
+                    reason="oracle/_ref not built")
+def test_bench_reference_arm_prints_exactly_one_json_line():
+    """The driver parses bench.py's stdout: one JSON line, nothing else
+    (library banners go to stderr)."""
+    import subprocess
+    import sys
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "1", "--warmup", "1", "--cpu-budget-flops", "1e9", "--help"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0 and res.stdout == ""  # --help text is not the result line
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "1",
+                          "--steps", "1", "--warmup", "1", "--cpu-budget-flops", "1e9"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = res.stdout.splitlines()
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
