@@ -394,15 +394,19 @@ def run_ours(args):
     eng.fold_nodes(text, out=host_nodes)
     host_x1 = [np.asarray([Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)],
                           dtype=np.int32) for i in range(args.steps)]
-    if world > 1:
-        torch.distributed.barrier()
-    t0 = time.perf_counter()
-    for i in range(args.steps):
+    def e2e_step(i):
         eng.load_nodes(host_nodes)
         if xb == 1:
             eng.amplitude_batch(host_x1[i][0], slices_for(args.warmup + i))
         else:
             eng.amplitude_batches(open_q, host_x1[i], slices_for(args.warmup + i), bitstrings=False)
+
+    e2e_step(0)  # untimed warm-up of the API path (pinned staging, graph key)
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_step(i)
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
