@@ -3,13 +3,16 @@
 amplitudes/sec and sustained Eq.(1) Tflop/s, with the roofline fraction, next
 to the reference CPU path on the same host).
 
-Default workload (N=1): BASELINE config 2 -- 7x7 grid RQC depth (1+32+1), the
-reference 7x7 region order with one cut bond (2 slices), a 1024-amplitude
-batch per x1 draw.  One "step" = one full amplitude batch (both slices) per
-GPU; N GPUs run independent x1 batches (weak scaling) and results meet in
-one NCCL all-gather at the end.
+Default workload (N=1): BASELINE config 5 -- 7x7 grid RQC depth (1+40+1),
+reference_plan_7x7 (1024 slices, rank-30 intermediates), the largest config
+that fits one GPU.  One "step" = one slice per GPU; the job is the ascending
+select_slices list, split into contiguous per-rank blocks, every rank on the
+same x1; a 64-amplitude batch needs 6 slices (fidelity 6/1024, the paper's
+run).  The per-slice contributions meet in one NCCL all-gather and an
+ascending-slice FP64 merge at the end (checked).  Config 2 (1024-amplitude
+batches, 2 slices) instead runs whole x1 batches per GPU.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1|2|5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 1|2|3|4|5]
 """
 from __future__ import annotations
 
@@ -141,10 +144,9 @@ def cpu_reference_sample(cfg, steps_prefix: int, threads: int, seed: int = 0, nt
     `steps_prefix` plan steps of `ntasks` (default: `threads`) independent
     (x1, slice) tasks on `threads` host threads.  Returns (seconds, flops)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import reflib
-    import paper_1905_00444_b200 as Q
+    import reflib  # the reference's own generator: nothing from libqsg.so on this arm
     r, c, m, s = cfg["circuit"]
-    text = Q.generate_rqc(r, c, m, s)
+    text = reflib.generate_rqc(r, c, m, s)
     plan = open(os.path.join(ROOT, cfg["plan"])).read()
     open_q = json.loads(plan)["open_qubits"]
     return reflib.execute_prefix(text, plan, open_q, steps_prefix, ntasks or threads, threads, seed)
@@ -235,6 +237,41 @@ def reference_prefix_steps(plan_json: dict, budget_flops: float) -> int:
     return n
 
 
+def host_cpu():
+    """(nproc, CPU model) of this host, reported next to every CPU number."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def reference_anchor():
+    """The composite model checked against one COMPLETE stock reference
+    slice (scripts/ref_anchor.py -> profiles/ref_anchor.json), if recorded."""
+    p = os.path.join(ROOT, "profiles", "ref_anchor.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return {k: d[k] for k in ("config", "measured_s", "model_s", "measured_over_model", "host", "note") if k in d}
+
+
+def cpu_baseline_record(value, threads, sample):
+    nproc, model = host_cpu()
+    rec = {"value": value, "unit": "amplitudes/s", "cores": threads, "kind": "reference", "extrapolated": True,
+           "nproc": nproc, "cpu_model": model, "sample": sample}
+    anchor = reference_anchor()
+    if anchor:
+        rec["anchor"] = anchor
+    return rec
+
+
 def run_reference_arm(args):
     world, rank, local = dist_setup()
     if rank != 0:
@@ -268,13 +305,15 @@ def run_reference_arm(args):
         "data": "synthetic (seeded RQC, random x1)",
         "config": {"workload": cfg["workload"], "parallelism": f"{threads} host threads"},
         "tflops_eq1": rate_eff / 1e12,
-        "cpu_baseline": {"value": amps, "unit": "amplitudes/s", "cores": threads, "kind": "reference",
-                         "sample": f"reference qsim kernels (contract_ttgt + normalize_inplace, Eigen GEMM via "
-                                   f"OpenBLAS 1-thread shim) over plan steps s000..s{nsteps - 1:03d} "
-                                   f"({prefix_flops / plan['per_slice']['flops']:.2%} of a slice's Eq.1 flops) of "
-                                   f"{ntasks} independent (x1, slice) tasks per step on {threads} threads at "
-                                   f"{rate / 1e9:.1f} Eq.1 Gflop/s; {heavy_desc}; amplitudes/s = batch / "
-                                   f"(heavy flops / heavy rate + other flops / prefix rate)"},
+        "cpu_baseline": cpu_baseline_record(
+            amps, threads,
+            f"EXTRAPOLATED: reference qsim kernels (contract_ttgt + normalize_inplace, Eigen GEMM via "
+            f"OpenBLAS 1-thread shim) over plan steps s000..s{nsteps - 1:03d} "
+            f"({prefix_flops / plan['per_slice']['flops']:.2%} of a slice's Eq.1 flops) of "
+            f"{ntasks} independent (x1, slice) tasks per step on {threads} threads at "
+            f"{rate / 1e9:.1f} Eq.1 Gflop/s; {heavy_desc}; amplitudes/s = batch / "
+            f"(heavy flops / heavy rate + other flops / prefix rate); ms_per_step is the timed sample, "
+            f"not a batch"),
         "e2e": {"value": amps, "unit": "amplitudes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -318,14 +357,26 @@ def run_ours(args):
     per_step = cfg["slices_per_step"] or K
     batch = xb * (1 << len(open_q))  # amplitudes delivered per run
 
+    from paper_1905_00444_b200 import distributed as D
+    slice_mode = cfg["slices_per_step"] is not None
+    if slice_mode:
+        # One sliced job: the ascending select_slices list of steps x world
+        # x per_step slices (src/engine.cpp:285-298), contiguous blocks per
+        # rank; every rank contracts the SAME x1 (draw 0).
+        njob = min(args.steps * world * per_step, K)
+        job_ids = Q.select_slices(njob, K, K, 0)
+        blocks = D.slice_blocks(job_ids, world)
+        mine = blocks[rank]
+
     def slices_for(step_index: int):
-        if cfg["slices_per_step"] is None:
+        """Slices of timed step `step_index` (warm-up steps reuse step 0's)."""
+        if not slice_mode:
             return list(range(K))
-        base = (rank * (args.steps + args.warmup) + step_index) * per_step
-        return [(base + j) % K for j in range(per_step)]
+        i = max(step_index - args.warmup, 0)
+        return [mine[(i * per_step + j) % len(mine)] for j in range(per_step)]
 
     # ---- device-timed region: node tensors resident, slices back to back ----
-    x1 = Q.draw_x1(n, open_q, 0, rank) if xb == 1 else [-1] * n
+    x1 = (Q.draw_x1(n, open_q, 0, 0 if slice_mode else rank) if xb == 1 else [-1] * n)
     eng.prepare(x1)
     eng.synchronize()
     for w in range(args.warmup):
@@ -341,6 +392,12 @@ def run_ours(args):
     # steps, outside the per-step event windows.
     small = info.arena_bytes < (256 << 20)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if small else None
+
+    def timed_run(i):
+        # batch mode: every step is a whole batch (reset); slice mode: the
+        # rank's block accumulates across steps, one per-slice row per slice.
+        eng.run(slices_for(args.warmup + i), reset=(not slice_mode or i == 0), per_slice=True)
+
     with ClockSampler(local) as clocks:
         if small:
             ms = 0.0
@@ -350,14 +407,14 @@ def run_ours(args):
                 for i in range(args.steps):
                     flush.fill_(i & 255)
                     evs[i][0].record(stream)
-                    eng.run(slices_for(args.warmup + i), reset=True, per_slice=True)
+                    timed_run(i)
                     evs[i][1].record(stream)
             torch.cuda.synchronize()
             ms = sum(a.elapsed_time(b) for a, b in evs)
         else:
             ev0.record(stream)
             for i in range(args.steps):
-                eng.run(slices_for(args.warmup + i), reset=True, per_slice=True)
+                timed_run(i)
             ev1.record(stream)
             ev1.synchronize()
             ms = ev0.elapsed_time(ev1)
@@ -373,15 +430,40 @@ def run_ours(args):
     flops_total = info.flops_per_slice * per_step * args.steps * world
     value = amps_total / (ms / 1e3)
     tflops = flops_total / (ms / 1e3) / 1e12
-    _, per_slice = eng.results()
+    amps_local, rows = eng.results(per_slice=True)
 
-    # ---- the one collective: all-gather every rank's last-step per-slice
-    # contributions (NCCL over NVLink), ordered FP64 merge on every rank.
-    merged_checksum = None
-    if world > 1:
-        from paper_1905_00444_b200 import distributed as D
-        allc = D.gather_contributions(per_slice, [per_slice.shape[0]] * world, device=torch.device("cuda", local))
-        merged_checksum = float(np.abs(D.ordered_merge(allc)).sum())
+    # ---- the one collective (NCCL over NVLink) and its checks.
+    merge = None
+    dev_t = torch.device("cuda", local)
+    if slice_mode:
+        # K3's FP64 accumulator over the rank's block == the ascending sum of
+        # its per-slice rows, bit for bit (src/engine.cpp:352-356 order).
+        local_ok = bool(np.array_equal(D.ordered_merge(rows), amps_local))
+        allc = D.gather_contributions(rows, [len(bk) for bk in blocks], device=dev_t) if world > 1 else rows
+        merged = D.ordered_merge(allc)
+        cross_ok = None
+        if world > 1:
+            # per-slice contributions do not depend on the GPU: rank 0
+            # recomputes rank 1's first slice and must match its row exactly,
+            # so the merged batch equals the single-GPU run bit for bit.
+            if rank == 0:
+                eng.run([blocks[1][0]], reset=True, per_slice=True)
+                _, chk = eng.results(per_slice=True)
+                cross_ok = bool(np.array_equal(chk[0], allc[len(blocks[0])]))
+            flags = torch.tensor([int(local_ok)], device=dev_t)
+            torch.distributed.all_reduce(flags, op=torch.distributed.ReduceOp.MIN)
+            local_ok = bool(flags.item())
+        if not local_ok or cross_ok is False:
+            raise SystemExit(f"sliced merge check failed (local {local_ok}, cross-GPU {cross_ok})")
+        merge = {"slices": len(job_ids), "x1_draw": 0, "per_rank_block": len(mine),
+                 "checks": "per-rank K3 sum == ordered sum of its per-slice rows (bit-exact)"
+                           + ("; rank 0 recomputed rank 1's first slice: bit-identical row" if world > 1 else ""),
+                 "amplitude_norm2": float(np.vdot(merged, merged).real)}
+        if world > 1:
+            merge["collective"] = "1x NCCL all_gather of per-slice FP64 contributions + ascending-slice merge"
+    elif world > 1:
+        D.gather_contributions(amps_local[None, :], [1] * world, device=dev_t)
+        merge = {"collective": "1x NCCL all_gather of the per-rank x1 batches (independent amplitude batches)"}
 
     # ---- end-to-end through the public API, every step: H2D of the circuit's
     # node tensors (the host open fold, pinned) -> Engine.load_nodes, host x1
@@ -392,7 +474,8 @@ def run_ours(args):
     # x1 draws, src/sampler.cpp:70-82) are made before the timed region
     host_nodes = torch.empty(info.node_bytes // 8, dtype=torch.complex64, pin_memory=True)
     eng.fold_nodes(text, out=host_nodes)
-    host_x1 = [np.asarray([Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)],
+    host_x1 = [np.asarray([Q.draw_x1(n, open_q, 0, 0) if slice_mode else
+                           Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)],
                           dtype=np.int32) for i in range(args.steps)]
     def e2e_step(i):
         eng.load_nodes(host_nodes)
@@ -470,12 +553,18 @@ def run_ours(args):
         roof["traffic_source"] = traffic["report"]
         roof["traffic_algorithmic"] = traffic["algorithmic_bytes"]
 
+    tc_share = sum(p["ms_total"] for p in gemms if p["tensor_cores"]) / max(total_ms, 1e-30)
+    if tc_share > 0.5:
+        dtype_label = (f"c64 (tcgen05 {split} split of fp32 operands, fp32 accumulate: "
+                       f"{tc_share:.0%} of the step; the rest FP32 FFMA / data movement)")
+    else:
+        dtype_label = (f"c64 (fp32 FFMA SIMT / narrow GEMMs; tensor cores {tc_share:.0%} of the step)")
     line = None
     if rank == 0:
         line = {
             "metric": "amplitudes_per_sec", "value": value, "unit": "amplitudes/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": ("c64 (tensor cores: 3xFP16 split of fp32 operands, fp32 accumulate)" if not args.no_tc else "c64 (fp32 FFMA)"),
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype_label,
             "data": "synthetic (seeded RQC from generate_rqc, random x1 via mt19937_64)",
             "config": {"workload": cfg["workload"], "parallelism": (f"x1 batches across {world} GPU(s)" if cfg["slices_per_step"] is None else f"slices across {world} GPU(s)"),
                        "amplitudes_per_step_per_gpu": batch, "slices_per_step_per_gpu": per_step,
@@ -495,8 +584,8 @@ def run_ours(args):
                             "through the Engine API; D2H = batch amplitudes"},
             "gpu_launches": launches, "clocks": clk, "roofline": roof,
         }
-        if merged_checksum is not None:
-            line["config"]["collective"] = "1x NCCL all_gather of per-slice FP64 contributions + ordered merge"
+        if merge is not None:
+            line["config"]["merge"] = merge
     if world > 1:
         torch.distributed.barrier()
     # CPU baseline: rank 0 at N=1 only.
@@ -511,12 +600,12 @@ def run_ours(args):
                                       else (rate, "no heavy steps beyond the prefix"))
             # the reference runs the plan as given: its flops and batch per x1 draw
             cpu_amps = cpu_composite_amps(plan, cfg, rate, heavy_rate, per_step, nsteps)
-            line["cpu_baseline"] = {
-                "value": cpu_amps, "unit": "amplitudes/s", "cores": cpu_threads, "kind": "reference",
-                "sample": f"unmodified reference kernels (oracle/_ref, Eigen->OpenBLAS 1-thread shim) over plan "
-                          f"steps s000..s{nsteps - 1:03d} of {ntasks} (x1, slice) tasks on {cpu_threads} "
-                          f"threads in {secs:.1f} s at {rate / 1e9:.1f} Eq.1 Gflop/s; {heavy_desc}; "
-                          f"amplitudes/s = batch / (heavy flops / heavy rate + other flops / prefix rate)"}
+            line["cpu_baseline"] = cpu_baseline_record(
+                cpu_amps, cpu_threads,
+                f"EXTRAPOLATED: unmodified reference kernels (oracle/_ref, Eigen->OpenBLAS 1-thread shim) over "
+                f"plan steps s000..s{nsteps - 1:03d} of {ntasks} (x1, slice) tasks on {cpu_threads} "
+                f"threads in {secs:.1f} s at {rate / 1e9:.1f} Eq.1 Gflop/s; {heavy_desc}; "
+                f"amplitudes/s = batch / (heavy flops / heavy rate + other flops / prefix rate)")
         except Exception as exc:  # reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "amplitudes/s", "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {exc}"}
@@ -547,8 +636,8 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(CONFIGS), default="2",
-                    help="BASELINE config: 1, 2 (default, the metric's workload), 3/4 (Bristlecone stand-ins), 5")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="5",
+                    help="BASELINE config: 5 (default: the largest single-GPU config), 1, 2, 3/4 (Bristlecone)")
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
     ap.add_argument("--reassociate", action="store_true",
                     help="opt-in contraction-tree rewrite of the plan (Q.reassociate_plan); off for the headline")

@@ -115,16 +115,21 @@ int qsg_cgemm_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, 
 /* K2 on the tcgen05 tensor cores at FP32-level accuracy: CTA-pair 3xFP16
  * with power-of-two operand scaling when m % 256 == 0 (the production
  * path), 3xTF32 otherwise (QSG_TC_PREC=tf32 forces it).  Requires
- * m % 128 == 0, 2n % 32 == 0, k % 16 == 0, A row-major; returns
- * QSG_ERR_INVALID_ARGUMENT otherwise.  Allocates its workspace (operand
- * maxima, B / A plane expansion) internally and synchronises the stream. */
+ * m % 128 == 0, 2n % 32 == 0, k % 16 == 0, A row-major.
+ * qsg_cgemm_tc_workspace_bytes returns the device scratch the call needs
+ * (operand maxima, K-sync counters, B / A fp16 planes), or -1 for an
+ * ineligible shape.  qsg_cgemm_tc_dev is stream-ordered and asynchronous:
+ * no allocation, no synchronisation; the caller owns `workspace_dev`
+ * (>= the returned size, reusable once the call has completed on `stream`).
+ * QSG_ERR_INVALID_ARGUMENT for an ineligible shape or a short workspace. */
+int64_t qsg_cgemm_tc_workspace_bytes(int64_t m, int64_t n, int64_t k, int trans_b);
 int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_b,
-                     void* stream);
+                     void* workspace_dev, int64_t workspace_bytes, void* stream);
 
 /* K3: acc[i] += double(fin[i]) * 2^log_scale for i < count (complex128
  * acc), and per_slice[i] = that contribution when per_slice_dev is not NULL.
  * The per-slice accumulation of batch_amplitudes (src/sampler.cpp:28-34).
- * Synchronises the stream. */
+ * Stream-ordered and asynchronous (log_scale is passed by value). */
 int qsg_accumulate_dev(const void* fin_dev, double log_scale, int64_t count, void* acc_dev, void* per_slice_dev,
                        void* stream);
 
@@ -214,7 +219,9 @@ int qsg_engine_fold_nodes(qsg_engine* e, const char* circuit_text, void* host_no
 int qsg_engine_load_nodes(qsg_engine* e, const void* host_nodes, int64_t bytes);
 int qsg_engine_export_nodes(qsg_engine* e, void* host_nodes, int64_t bytes);
 /* Run slices (async, engine stream).  reset: zero the batch accumulator;
- * per_slice: keep each slice's contribution. */
+ * per_slice: keep each slice's contribution (appended after the previous
+ * run's rows when reset = 0 and that run kept rows, so a batch split over
+ * several runs keeps one row per slice in run order). */
 int qsg_engine_run(qsg_engine* e, const int64_t* slice_ids, int64_t k, int reset, int per_slice);
 /* Batch amplitudes (batch_size complex128) and, if non-null, per-slice
  * contributions (k x batch_size complex128); synchronises. */
@@ -222,6 +229,11 @@ int qsg_engine_results(qsg_engine* e, double* amps_host, double* per_slice_host)
 int qsg_engine_stream(qsg_engine* e, void** stream);
 int qsg_engine_synchronize(qsg_engine* e);
 int qsg_engine_launches(qsg_engine* e, int64_t* launches);
+/* Rows (slices) of per-slice contributions kept by the engine's last run
+ * (0 when that run -- including the internal runs of qsg_amplitude_batch,
+ * qsg_run_amplitudes, qsg_sample -- did not keep them); per_slice_host of
+ * qsg_engine_results receives rows x batch_size complex128 values. */
+int qsg_engine_per_slice_rows(qsg_engine* e, int64_t* rows);
 
 typedef struct qsg_op_profile {
   int32_t kind;  /* 0 permute, 1 gemm, 2 accumulate */

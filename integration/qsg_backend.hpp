@@ -21,10 +21,11 @@ inline void check(int rc) {
     default: throw std::runtime_error(m);
   }
 }
-// Drop-in for contract_ttgt + normalize_inplace on host tensors
-// (contraction.hpp:186 / tensor.hpp:209): labels -> small ints.
-inline Tensorf contract_normalized(const Tensorf& l, const Tensorf& r, const std::vector<Label>& out_labels,
-                                   FlopCounter* fc) {
+// Drop-in for contract_ttgt (contraction.hpp:186), followed by
+// normalize_inplace (tensor.hpp:209) when `normalize`, on host tensors:
+// labels -> small ints; the contraction runs on the GPU.
+inline Tensorf contract(const Tensorf& l, const Tensorf& r, const std::vector<Label>& out_labels, FlopCounter* fc,
+                        bool normalize) {
   std::map<Label, int> id;
   auto ids = [&](const std::vector<Label>& ls) { std::vector<int> v; for (auto& x : ls) v.push_back(id.emplace(x, id.size()).first->second); return v; };
   auto li = ids(l.labels()), ri = ids(r.labels()), oi = ids(out_labels);
@@ -33,8 +34,12 @@ inline Tensorf contract_normalized(const Tensorf& l, const Tensorf& r, const std
   double scale = 0; std::uint64_t flops = 0;
   check(qsg_contract(l.rank(), li.data(), l.dims().data(), reinterpret_cast<const float*>(l.data().data()), l.log_scale(),
                      r.rank(), ri.data(), r.dims().data(), reinterpret_cast<const float*>(r.data().data()), r.log_scale(),
-                     (int)oi.size(), oi.data(), reinterpret_cast<float*>(out.data()), &scale, &flops, 1));
+                     (int)oi.size(), oi.data(), reinterpret_cast<float*>(out.data()), &scale, &flops, normalize ? 1 : 0));
   if (fc) fc->add(flops);
   return Tensorf(out_labels, od, std::move(out), scale);
+}
+inline Tensorf contract_normalized(const Tensorf& l, const Tensorf& r, const std::vector<Label>& out_labels,
+                                   FlopCounter* fc) {
+  return contract(l, r, out_labels, fc, true);
 }
 }  // namespace qsim::qsg_backend

@@ -14,7 +14,11 @@ import struct
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_ref", "libqsim_ref.so")
+# QSIM_REF_LIB selects another build of the same library, e.g.
+# _ref/libqsim_relink.so (the reference relinked onto libqsg.so,
+# oracle/Makefile `relink`).
+LIB_PATH = os.environ.get("QSIM_REF_LIB") or os.path.join(_HERE, "_ref", "libqsim_ref.so")
+RELINK_PATH = os.path.join(_HERE, "_ref", "libqsim_relink.so")
 
 _lib = None
 

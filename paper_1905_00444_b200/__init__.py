@@ -117,7 +117,8 @@ def lib():
         "qsg_draw_x1": (i32, [i32, P(i32), i32, u64, u64, P(i32)]),
         "qsg_permute_dev": (i32, [vp, i64, vp, i32, P(i64), P(i64), vp]),
         "qsg_cgemm_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, i32, vp]),
-        "qsg_cgemm_tc_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, vp]),
+        "qsg_cgemm_tc_workspace_bytes": (i64, [i64, i64, i64, i32]),
+        "qsg_cgemm_tc_dev": (i32, [vp, vp, vp, i64, i64, i64, i32, vp, i64, vp]),
         "qsg_accumulate_dev": (i32, [vp, C.c_double, i64, vp, vp, vp]),
         "qsg_transpose": (i32, [i32, P(i64), fp, P(i32), fp]),
         "qsg_contract": (i32, [i32, P(i32), P(i64), fp, C.c_double, i32, P(i32), P(i64), fp, C.c_double, i32, P(i32),
@@ -141,6 +142,7 @@ def lib():
         "qsg_engine_stream": (i32, [vp, P(vp)]),
         "qsg_engine_synchronize": (i32, [vp]),
         "qsg_engine_launches": (i32, [vp, P(i64)]),
+        "qsg_engine_per_slice_rows": (i32, [vp, P(i64)]),
         "qsg_engine_profile": (i32, [vp, P(_OpProfile), i32, P(i32)]),
         "qsg_engine_reset_profile": (i32, [vp]),
         "qsg_engine_set_profile": (i32, [vp, i32]),
@@ -509,19 +511,28 @@ class Engine:
 
     def run(self, slice_ids, reset: bool = True, per_slice: bool = False):
         ids = np.ascontiguousarray(np.asarray(list(slice_ids), dtype=np.int64))
-        self._last_k = len(ids)
-        self._per_slice = per_slice
         _check(lib().qsg_engine_run(self._h, _p(ids, C.c_int64), len(ids), 1 if reset else 0, 1 if per_slice else 0))
 
-    def results(self):
+    def per_slice_rows(self) -> int:
+        """Slices whose contributions the engine's last run kept (0 if none)."""
+        n = C.c_int64(0)
+        _check(lib().qsg_engine_per_slice_rows(self._h, C.byref(n)))
+        return n.value
+
+    def results(self, per_slice=None):
+        """Amplitudes of the last run; with per-slice contributions as well when
+        that run kept them (or always when per_slice=True, which raises if the
+        last run -- e.g. an internal amplitude_batch -- did not)."""
+        rows = self.per_slice_rows()
+        if per_slice and rows == 0:
+            raise InvalidArgument("results: the last run kept no per-slice contributions")
+        want = rows > 0 if per_slice is None else bool(per_slice)
         amps = np.zeros(2 * self.info.batch_size, dtype=np.float64)
-        ps = None
-        if getattr(self, "_per_slice", False):
-            ps = np.zeros(2 * self.info.batch_size * self._last_k, dtype=np.float64)
+        ps = np.zeros(2 * self.info.batch_size * rows, dtype=np.float64) if want else None
         _check(lib().qsg_engine_results(self._h, _p(amps, C.c_double), _p(ps, C.c_double) if ps is not None else None))
         out = amps.view(np.complex128)
         if ps is not None:
-            return out, ps.view(np.complex128).reshape(self._last_k, self.info.batch_size)
+            return out, ps.view(np.complex128).reshape(rows, self.info.batch_size)
         return out
 
     def stream(self) -> int:

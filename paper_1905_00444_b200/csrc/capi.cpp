@@ -265,13 +265,19 @@ int qsg_cgemm_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, 
   });
 }
 
+int64_t qsg_cgemm_tc_workspace_bytes(int64_t m, int64_t n, int64_t k, int trans_b) {
+  if (m <= 0 || n <= 0 || k <= 0 || !qsg::dev::cgemm_tc_supported(m, n, k, false, trans_b != 0)) return -1;
+  return qsg::dev::cgemm_tc_workspace_bytes(m, n, k, false, trans_b != 0);
+}
+
 int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t m, int64_t n, int64_t k, int trans_b,
-                     void* stream) {
+                     void* workspace_dev, int64_t workspace_bytes, void* stream) {
   return guarded([&] {
     if (!qsg::dev::cgemm_tc_supported(m, n, k, false, trans_b != 0))
       throw std::invalid_argument("cgemm_tc: shape not eligible for the tensor-core path");
     const std::int64_t ws = qsg::dev::cgemm_tc_workspace_bytes(m, n, k, false, trans_b != 0);
-    DevBuf w(static_cast<std::size_t>(ws));
+    if (workspace_dev == nullptr || workspace_bytes < ws)
+      throw std::invalid_argument("cgemm_tc: workspace smaller than qsg_cgemm_tc_workspace_bytes()");
     qsg::dev::GemmArgs g{};
     g.a = a_dev;
     g.b = b_dev;
@@ -280,11 +286,9 @@ int qsg_cgemm_tc_dev(const void* a_dev, const void* b_dev, void* c_dev, int64_t 
     g.n = n;
     g.k = k;
     g.trans_b = trans_b != 0;
-    g.workspace = w.p;
-    g.workspace_bytes = ws;
-    auto s = static_cast<cudaStream_t>(stream);
-    cuda_check(qsg::dev::cgemm_tc(g, s), "cgemm_tc");
-    cuda_check(cudaStreamSynchronize(s), "cgemm_tc sync");
+    g.workspace = workspace_dev;
+    g.workspace_bytes = workspace_bytes;
+    cuda_check(qsg::dev::cgemm_tc(g, static_cast<cudaStream_t>(stream)), "cgemm_tc");
   });
 }
 
@@ -292,14 +296,8 @@ int qsg_accumulate_dev(const void* fin_dev, double log_scale, int64_t count, voi
                        void* stream) {
   return guarded([&] {
     if (count < 0) throw std::invalid_argument("accumulate: negative count");
-    DevBuf meta(sizeof(qsg::dev::TMeta));
-    qsg::dev::TMeta h{};
-    h.log_scale = log_scale;
-    auto s = static_cast<cudaStream_t>(stream);
-    cuda_check(cudaMemcpyAsync(meta.p, &h, sizeof h, cudaMemcpyHostToDevice, s), "H2D");
-    cuda_check(qsg::dev::accumulate(fin_dev, meta.as<qsg::dev::TMeta>(), count, acc_dev, per_slice_dev, s),
+    cuda_check(qsg::dev::accumulate(fin_dev, log_scale, count, acc_dev, per_slice_dev, static_cast<cudaStream_t>(stream)),
                "accumulate");
-    cuda_check(cudaStreamSynchronize(s), "accumulate sync");
   });
 }
 
@@ -593,6 +591,10 @@ int qsg_engine_stream(qsg_engine* e, void** stream) {
 
 int qsg_engine_synchronize(qsg_engine* e) {
   return guarded([&] { e->impl->synchronize(); });
+}
+
+int qsg_engine_per_slice_rows(qsg_engine* e, int64_t* rows) {
+  return guarded([&] { *rows = e->impl->per_slice_rows(); });
 }
 
 int qsg_engine_launches(qsg_engine* e, int64_t* launches) {

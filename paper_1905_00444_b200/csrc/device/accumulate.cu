@@ -18,9 +18,10 @@ namespace {
 constexpr int NT = 256;
 
 __global__ void __launch_bounds__(NT) accumulate_kernel(const float2* __restrict__ fin, const TMeta* meta,
-                                                        long long count, double2* __restrict__ acc,
+                                                        double log_scale, long long count,
+                                                        double2* __restrict__ acc,
                                                         double2* __restrict__ per_slice) {
-  const double scale = exp2(meta->log_scale);
+  const double scale = exp2(meta ? meta->log_scale : log_scale);
   for (long long i = blockIdx.x * static_cast<long long>(NT) + threadIdx.x; i < count;
        i += static_cast<long long>(gridDim.x) * NT) {
     const float2 v = fin[i];
@@ -73,7 +74,16 @@ unsigned grid_for(long long count) {
 cudaError_t accumulate(const void* fin, const TMeta* meta, std::int64_t count, void* acc, void* per_slice,
                        cudaStream_t stream, int* launches) {
   if (count <= 0) return cudaSuccess;
-  accumulate_kernel<<<grid_for(count), NT, 0, stream>>>(static_cast<const float2*>(fin), meta, count,
+  accumulate_kernel<<<grid_for(count), NT, 0, stream>>>(static_cast<const float2*>(fin), meta, 0.0, count,
+                                                        static_cast<double2*>(acc), static_cast<double2*>(per_slice));
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t accumulate(const void* fin, double log_scale, std::int64_t count, void* acc, void* per_slice,
+                       cudaStream_t stream, int* launches) {
+  if (count <= 0) return cudaSuccess;
+  accumulate_kernel<<<grid_for(count), NT, 0, stream>>>(static_cast<const float2*>(fin), nullptr, log_scale, count,
                                                         static_cast<double2*>(acc), static_cast<double2*>(per_slice));
   if (launches) ++*launches;
   return cudaGetLastError();

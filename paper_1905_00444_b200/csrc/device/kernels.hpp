@@ -83,6 +83,9 @@ cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches = nullpt
 // per_slice (nullable) receives contrib.
 cudaError_t accumulate(const void* fin, const TMeta* meta, std::int64_t count, void* acc_double2,
                        void* per_slice_double2, cudaStream_t stream, int* launches = nullptr);
+// Same with a host-side log_scale (C ABI qsg_accumulate_dev: no device meta).
+cudaError_t accumulate(const void* fin, double log_scale, std::int64_t count, void* acc_double2,
+                       void* per_slice_double2, cudaStream_t stream, int* launches = nullptr);
 
 // ---- normalisation helpers (standalone normalize_inplace) --------------------
 // max |z|^2 into meta->maxsq_bits (atomicMax; zero it first).

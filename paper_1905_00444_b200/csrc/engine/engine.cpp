@@ -881,21 +881,37 @@ std::vector<std::int64_t> Engine::run_key(const std::vector<std::int64_t>& slice
   key.push_back(reset ? 1 : 0);
   key.push_back(per_slice ? 1 : 0);
   key.push_back(reinterpret_cast<std::int64_t>(per_slice_));
+  key.push_back(per_slice_base_);
   return key;
 }
 
 void Engine::run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) {
   check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  // Validate every id before anything is queued or captured: a bad id must
+  // neither leave the accumulator half-updated nor poison graph capture.
+  for (const auto id : slice_ids) (void)cut_digits(shape_, plan_.cut, id);
   if (per_slice) {
-    const std::int64_t need = static_cast<std::int64_t>(slice_ids.size()) * batch_;
+    // Rows append after the previous run's when the accumulator is kept
+    // (reset = false): K runs of one slice each leave K rows, in run order.
+    const std::int64_t base = (!reset && per_slice_used_ > 0) ? per_slice_used_ : 0;
+    const std::int64_t need = (base + static_cast<std::int64_t>(slice_ids.size())) * batch_;
     if (need > per_slice_cap_) {
+      const std::int64_t cap = std::max(need, 2 * per_slice_cap_);
+      double2* grown = nullptr;
+      check(cudaMalloc(&grown, sizeof(double2) * static_cast<std::size_t>(cap)), "per-slice cudaMalloc");
+      if (base > 0)
+        check(cudaMemcpyAsync(grown, per_slice_, sizeof(double2) * static_cast<std::size_t>(base * batch_),
+                              cudaMemcpyDeviceToDevice, stream_),
+              "per-slice copy");
       check(cudaStreamSynchronize(stream_), "sync");
       if (per_slice_) cudaFree(per_slice_);
-      check(cudaMalloc(&per_slice_, sizeof(double2) * static_cast<std::size_t>(need)), "per-slice cudaMalloc");
-      per_slice_cap_ = need;
+      per_slice_ = grown;
+      per_slice_cap_ = cap;
     }
-    per_slice_used_ = static_cast<std::int64_t>(slice_ids.size());
+    per_slice_base_ = base;
+    per_slice_used_ = base + static_cast<std::int64_t>(slice_ids.size());
   } else {
+    per_slice_base_ = 0;
     per_slice_used_ = 0;
   }
   if (events_pending_) profile();  // fold finished timings before reusing events
@@ -963,7 +979,8 @@ void Engine::enqueue_run(const std::vector<std::int64_t>& slice_ids, bool reset,
         if (ax >= 0) node_off[q] += digits[ci] * node_full_strides_[q][static_cast<std::size_t>(ax)];
       }
     check(cudaMemsetAsync(metas_, 0, sizeof(dev::TMeta) * static_cast<std::size_t>(nmeta_), stream_), "meta reset");
-    void* slot = per_slice ? static_cast<void*>(per_slice_ + static_cast<std::int64_t>(s) * batch_) : nullptr;
+    void* slot =
+        per_slice ? static_cast<void*>(per_slice_ + (per_slice_base_ + static_cast<std::int64_t>(s)) * batch_) : nullptr;
     for (std::size_t i = 0; i < ops_.size(); ++i) {
       launch_op(i, node_off, slot);
     }

@@ -115,6 +115,8 @@ class Engine {
   void synchronize();
 
   std::int64_t launches() const { return launches_; }
+  // Rows of per-slice contributions the last run() kept (0 without per_slice).
+  std::int64_t per_slice_rows() const { return per_slice_used_; }
   std::vector<OpProfile> profile();  // synchronises
   void reset_profile();
   void set_profile(bool on);
@@ -217,6 +219,7 @@ class Engine {
   double2* per_slice_ = nullptr;
   std::int64_t per_slice_cap_ = 0;
   std::int64_t per_slice_used_ = 0;
+  std::int64_t per_slice_base_ = 0;  // first row the current run writes
   std::int64_t launches_ = 0;
   // CUDA graph of the last repeated run (see EngineOptions::graphs).
   void enqueue_run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice);

@@ -25,7 +25,10 @@ def gemm_err(m, n, k, seed=0, scale_spread=False):
     want = A.to(torch.complex128) @ B.to(torch.complex128)
     dA, dB = A.cuda(), B.cuda()
     out = {}
-    for name, fn in (("tc", lambda c: Q.lib().qsg_cgemm_tc_dev(dA.data_ptr(), dB.data_ptr(), c.data_ptr(), m, n, k, 0, None)),
+    wsb = int(Q.lib().qsg_cgemm_tc_workspace_bytes(m, n, k, 0))
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+    for name, fn in (("tc", lambda c: Q.lib().qsg_cgemm_tc_dev(dA.data_ptr(), dB.data_ptr(), c.data_ptr(), m, n, k, 0,
+                                                               ws.data_ptr(), wsb, None)),
                      ("simt", lambda c: Q.lib().qsg_cgemm_dev(dA.data_ptr(), dB.data_ptr(), c.data_ptr(), m, n, k, 0, 0, None))):
         c = torch.zeros(m, n, dtype=torch.complex64, device="cuda")
         Q._check(fn(c))

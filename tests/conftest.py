@@ -51,3 +51,14 @@ def sweep_plan(Q, rows, cols, m, seed, nopen):
     opn = sorted((rows - 1) * cols + c for c in range(nopen))
     draft = {"version": 1, "open_qubits": opn, "cut": {"labels": [], "group": 1}, "order": order}
     return text, Q.plan_json(text, opn, Q.PLAN_JSON, json.dumps(draft)), opn
+
+
+def tc_gemm(Q, a_ptr, b_ptr, c_ptr, m, n, k, trans_b=0):
+    """qsg_cgemm_tc_dev with a caller-owned workspace (the C ABI allocates
+    nothing and does not synchronise); synchronises here for the check."""
+    import torch
+    nbytes = int(Q.lib().qsg_cgemm_tc_workspace_bytes(m, n, k, trans_b))
+    assert nbytes >= 0, "shape not eligible for the tensor-core path"
+    ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+    Q._check(Q.lib().qsg_cgemm_tc_dev(a_ptr, b_ptr, c_ptr, m, n, k, trans_b, ws.data_ptr(), nbytes, None))
+    torch.cuda.synchronize()

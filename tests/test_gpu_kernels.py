@@ -9,7 +9,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN
+from conftest import GOLDEN, tc_gemm
 
 pytestmark = pytest.mark.gpu
 
@@ -160,7 +160,7 @@ def test_cgemm_tensor_core_vs_fp64(gpu, m, n, k, tb, prec, monkeypatch):
     dA = A.cuda()
     dB = (B.t().contiguous() if tb else B).cuda()
     dC = torch.zeros(m, n, dtype=torch.complex64, device="cuda")
-    gpu._check(gpu.lib().qsg_cgemm_tc_dev(dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), m, n, k, tb, None))
+    tc_gemm(gpu, dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), m, n, k, tb)
     torch.cuda.synchronize()
     got = dC.cpu().to(torch.complex128)
     err = float((got - want).abs().norm() / want.abs().norm())
@@ -188,7 +188,8 @@ def test_cgemm_tensor_core_dynamic_range(gpu, prec, monkeypatch):
     A = A * rs[:, None]
     want = A.to(torch.complex128) @ B.to(torch.complex128)
     dC = torch.zeros(m, n, dtype=torch.complex64, device="cuda")
-    gpu._check(gpu.lib().qsg_cgemm_tc_dev(A.cuda().data_ptr(), B.cuda().data_ptr(), dC.data_ptr(), m, n, k, 0, None))
+    dA, dB = A.cuda(), B.cuda()
+    tc_gemm(gpu, dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), m, n, k, 0)
     torch.cuda.synchronize()
     got = dC.cpu().to(torch.complex128)
     row_err = (got - want).abs().norm(dim=1) / want.abs().norm(dim=1)
@@ -207,6 +208,7 @@ def test_accumulate_kernel_matches_fp64(gpu):
     acc = torch.ones(1024, dtype=torch.complex128, device="cuda")
     per = torch.zeros(1024, dtype=torch.complex128, device="cuda")
     gpu._check(gpu.lib().qsg_accumulate_dev(fin.data_ptr(), -3.0, 1024, acc.data_ptr(), per.data_ptr(), None))
+    torch.cuda.synchronize()
     want = fin.cpu().to(torch.complex128) * 2.0 ** -3
     assert torch.equal(per.cpu(), want)
     assert torch.equal(acc.cpu(), want + 1)
