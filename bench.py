@@ -38,19 +38,53 @@ CONFIGS = {
           "workload": "config2: 7x7 RQC depth (1+32+1), reference 7x7 region order, 1 cut bond "
                       "b_007_003_004 (2 slices), 1024-amplitude batch per x1 draw",
           "slices_per_step": None},
-    "3": {"circuit": (6, 10, 32, 0), "plan": "configs/config3_standin_6x10_plan.json",
-          "workload": "config3 stand-in for Bristlecone-60: 6x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
-                      "(4096 slices), closed amplitude over a fixed 2^10-slice subset; 1 slice per step per GPU",
+    "3": {"circuit": (11, 12, 32, 0), "mask": 60, "plan": "configs/config3_bristlecone60_plan.json",
+          "workload": "config3: Bristlecone-60 (11x12 diamond embedding) depth (1+32+1), column snake, 10 cut bonds "
+                      "(1024 slices), closed amplitude over the fixed 2^10-slice set; 1 slice per step per GPU",
           "slices_per_step": 1, "slices_per_batch": 1024},
-    "4": {"circuit": (7, 10, 32, 0), "plan": "configs/config4_standin_7x10_plan.json",
-          "workload": "config4 stand-in for Bristlecone-70: 7x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
-                      "(4096 slices), closed amplitude over a fixed 2^12-slice subset; 1 slice per step per GPU",
+    "4": {"circuit": (11, 12, 32, 0), "mask": 70, "plan": "configs/config4_bristlecone70_plan.json",
+          "workload": "config4: Bristlecone-70 (11x12 diamond embedding) depth (1+32+1), column snake, 16 cut bonds "
+                      "(65536 slices, max rank 32), closed amplitude over a fixed 2^12-slice subset; 1 slice per "
+                      "step per GPU",
           "slices_per_step": 1, "slices_per_batch": 4096},
+    "3s": {"circuit": (6, 10, 32, 0), "plan": "configs/config3_standin_6x10_plan.json",
+           "workload": "config3 rectangular stand-in: 6x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
+                       "(4096 slices), closed amplitude over a fixed 2^10-slice subset; 1 slice per step per GPU",
+           "slices_per_step": 1, "slices_per_batch": 1024},
+    "4s": {"circuit": (7, 10, 32, 0), "plan": "configs/config4_standin_7x10_plan.json",
+           "workload": "config4 rectangular stand-in: 7x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
+                       "(4096 slices), closed amplitude over a fixed 2^12-slice subset; 1 slice per step per GPU",
+           "slices_per_step": 1, "slices_per_batch": 4096},
     "5": {"circuit": (7, 7, 40, 0), "plan": "configs/config5_plan.json",
           "workload": "config5: 7x7 RQC depth (1+40+1), reference_plan_7x7 (1024 slices), 64-amplitude batch at "
                       "fidelity 6/1024 (6 slices per batch, as the paper's run); 1 slice per step per GPU",
           "slices_per_step": 1, "slices_per_batch": 6},
 }
+
+
+def circuit_text(cfg, gen):
+    """The config's circuit: generate_rqc (gen = the product's or the
+    reference's generator), or for the Bristlecone configs the masked 11x12
+    embedding committed as text (tests/golden/bristlecone{60,70}_circuit.txt,
+    written by generate_rqc_masked; the reference has no masked generator)."""
+    r, c, m, s = cfg["circuit"]
+    if "mask" in cfg:
+        with open(os.path.join(ROOT, "tests", "golden", f"bristlecone{cfg['mask']}_circuit.txt")) as f:
+            return f.read()
+    return gen(r, c, m, s)
+
+
+def idle_qubits(cfg):
+    """Cells outside the Bristlecone mask: H . H = identity, so their output bit must be 0."""
+    if "mask" not in cfg:
+        return []
+    text = circuit_text(cfg, None)
+    used = set()
+    for ln in text.splitlines()[1:]:
+        f = ln.split()
+        if len(f) >= 3 and not ln.startswith("#") and f[1] != "h":
+            used.update(int(x) for x in f[2:])
+    return [q for q in range(int(text.split()[0])) if q not in used]
 
 
 def tc_split(step):
@@ -145,8 +179,7 @@ def cpu_reference_sample(cfg, steps_prefix: int, threads: int, seed: int = 0, nt
     (x1, slice) tasks on `threads` host threads.  Returns (seconds, flops)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import reflib  # the reference's own generator: nothing from libqsg.so on this arm
-    r, c, m, s = cfg["circuit"]
-    text = reflib.generate_rqc(r, c, m, s)
+    text = circuit_text(cfg, reflib.generate_rqc)
     plan = open(os.path.join(ROOT, cfg["plan"])).read()
     open_q = json.loads(plan)["open_qubits"]
     return reflib.execute_prefix(text, plan, open_q, steps_prefix, ntasks or threads, threads, seed)
@@ -335,7 +368,8 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
     r, c, m, s = cfg["circuit"]
-    text = Q.generate_rqc(r, c, m, s)
+    text = circuit_text(cfg, Q.generate_rqc)
+    idle = idle_qubits(cfg)
     plan_text = open(os.path.join(ROOT, cfg["plan"])).read()
     plan = json.loads(plan_text)
     rewrites = None
@@ -376,7 +410,13 @@ def run_ours(args):
         return [mine[(i * per_step + j) % len(mine)] for j in range(per_step)]
 
     # ---- device-timed region: node tensors resident, slices back to back ----
-    x1 = (Q.draw_x1(n, open_q, 0, 0 if slice_mode else rank) if xb == 1 else [-1] * n)
+    def draw(seed, index):
+        x = Q.draw_x1(n, open_q, seed, index)
+        for q in idle:  # idle Bristlecone cells end in |0>
+            x[q] = 0
+        return x
+
+    x1 = (draw(0, 0 if slice_mode else rank) if xb == 1 else [-1] * n)
     eng.prepare(x1)
     eng.synchronize()
     for w in range(args.warmup):
@@ -474,8 +514,8 @@ def run_ours(args):
     # x1 draws, src/sampler.cpp:70-82) are made before the timed region
     host_nodes = torch.empty(info.node_bytes // 8, dtype=torch.complex64, pin_memory=True)
     eng.fold_nodes(text, out=host_nodes)
-    host_x1 = [np.asarray([Q.draw_x1(n, open_q, 0, 0) if slice_mode else
-                           Q.draw_x1(n, open_q, 1, (rank * args.steps + i) * xb + t) for t in range(xb)],
+    host_x1 = [np.asarray([draw(0, 0) if slice_mode else
+                           draw(1, (rank * args.steps + i) * xb + t) for t in range(xb)],
                           dtype=np.int32) for i in range(args.steps)]
     def e2e_step(i):
         eng.load_nodes(host_nodes)
@@ -637,7 +677,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="5",
-                    help="BASELINE config: 5 (default: the largest single-GPU config), 1, 2, 3/4 (Bristlecone)")
+                    help="BASELINE config: 5 (default: the largest single-GPU config), 1, 2, 3/4 (Bristlecone-60/70), "
+                         "3s/4s (rectangular stand-ins)")
     ap.add_argument("--no-tc", action="store_true", help="disable the tcgen05 GEMM path")
     ap.add_argument("--reassociate", action="store_true",
                     help="opt-in contraction-tree rewrite of the plan (Q.reassociate_plan); off for the headline")

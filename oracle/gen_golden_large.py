@@ -45,6 +45,10 @@ JOBS = {
                  "bitstrings": 2, "slices": [0, 1]},
     "config4s": {"circuit": (7, 10, 32, 0), "plan": "configs/config4_standin_7x10_plan.json",
                  "bitstrings": 1, "slices": [0]},
+    # Bristlecone-60 on the masked 11x12 embedding (circuit text committed
+    # under tests/golden/; parsed by the reference's own parse_circuit).
+    "bc60": {"circuit": (11, 12, 32, 0), "mask": 60, "plan": "configs/config3_bristlecone60_plan.json",
+             "bitstrings": 1, "slices": [0, 1]},
 }
 
 
@@ -62,7 +66,11 @@ def cpu_model() -> str:
 def run(name: str, threads: int) -> None:
     job = JOBS[name]
     r, c, m, seed = job["circuit"]
-    text = R.generate_rqc(r, c, m, seed)
+    if "mask" in job:
+        with open(os.path.join(GOLD, f"bristlecone{job['mask']}_circuit.txt")) as f:
+            text = f.read()
+    else:
+        text = R.generate_rqc(r, c, m, seed)
     plan_text = open(os.path.join(ROOT, job["plan"])).read()
     plan = json.loads(plan_text)
     n = r * c
@@ -73,6 +81,13 @@ def run(name: str, threads: int) -> None:
     else:  # closed plan: full bitstrings (closed qubits = x1), fixed numpy stream
         rng = np.random.default_rng(1905)
         x1s = [[int(b) for b in rng.integers(0, 2, n)] for _ in range(job["bitstrings"])]
+        if "mask" in job:  # idle cells (H . H) end in |0>
+            used = {int(q) for ln in text.splitlines()[1:] if not ln.startswith("#")
+                    for q in ln.split()[2:] if ln.split()[1] != "h"}
+            for x in x1s:
+                for q in range(n):
+                    if q not in used:
+                        x[q] = 0
     out = {}
     meta = {"name": name, "circuit": list(job["circuit"]), "plan": job["plan"], "slices": job["slices"],
             "x1": x1s, "blas_threads": threads, "cpu": cpu_model(), "nproc": os.cpu_count(),

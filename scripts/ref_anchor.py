@@ -9,7 +9,7 @@ Runs on the host it reports (here or the GPU box, via oracle/_ref):
             prefix + scaled-down heavy GEMM rate).
 Writes profiles/ref_anchor.json; bench.py attaches it to every cpu_baseline.
 
-    python scripts/ref_anchor.py [--config 3]
+    python scripts/ref_anchor.py [--config 3s]
 """
 from __future__ import annotations
 
@@ -29,16 +29,15 @@ import reflib  # noqa: E402
 
 def main() -> None:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="3")
+    ap.add_argument("--config", default="3s")
     ap.add_argument("--budget-flops", type=float, default=4e11)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "ref_anchor.json"))
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     plan_text = open(os.path.join(ROOT, cfg["plan"])).read()
     plan = json.loads(plan_text)
-    r, c, m, seed = cfg["circuit"]
-    text = reflib.generate_rqc(r, c, m, seed)
-    n = r * c
+    text = bench.circuit_text(cfg, reflib.generate_rqc)
+    n = int(text.split()[0])
     reflib.lib().ref_set_blas_threads(1)
 
     # model on one thread (exactly bench.py's composite)
