@@ -42,6 +42,7 @@ struct KParams {
   float2* c;
   float2* partial;  // split-K partials [splits][m][n] or null
   long long m, n, k, kchunk;
+  long long m_tiles;  // tiles are linearised over grid.x, m fastest (no 65535 grid.y limit)
   const TMeta* meta_a;
   const TMeta* meta_b;
   TMeta* meta_c;
@@ -73,8 +74,8 @@ __global__ void __launch_bounds__(NT, 2) cgemm_simt_kernel(const KParams p) {
   __shared__ __align__(16) float2 As[2][BK][BM + 2];
   __shared__ __align__(16) float2 Bs[2][BK][BN + 2];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const long long m0 = static_cast<long long>(blockIdx.x) * BM;
-  const long long n0 = static_cast<long long>(blockIdx.y) * BN;
+  const long long m0 = (static_cast<long long>(blockIdx.x) % p.m_tiles) * BM;
+  const long long n0 = (static_cast<long long>(blockIdx.x) / p.m_tiles) * BN;
   const long long kbeg = static_cast<long long>(blockIdx.z) * p.kchunk;
   const long long kend = min(p.k, kbeg + p.kchunk);
   const long long M = p.m, N = p.n, K = p.k;
@@ -374,8 +375,9 @@ cudaError_t cgemm(const GemmArgs& g, cudaStream_t stream, int* launches) {
   }
   p.kchunk = std::max<std::int64_t>(kchunk, 1);
   const std::int64_t gx = (g.m + BM - 1) / BM, gy = (g.n + BN - 1) / BN;
-  if (gy > 65535) throw std::length_error("cgemm: n too large for the grid");
-  dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(gy), static_cast<unsigned>(splits));
+  if (gx * gy > 0x7fffffff) throw std::length_error("cgemm: m x n too large for the grid");
+  p.m_tiles = gx;
+  dim3 grid(static_cast<unsigned>(gx * gy), 1, static_cast<unsigned>(splits));
   if (g.trans_a) {
     if (g.trans_b) cgemm_simt_kernel<true, true><<<grid, NT, 0, stream>>>(p);
     else cgemm_simt_kernel<true, false><<<grid, NT, 0, stream>>>(p);

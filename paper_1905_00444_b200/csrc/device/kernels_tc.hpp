@@ -1,5 +1,8 @@
-// K2 tensor-core path: complex64 GEMM as a real GEMM on tcgen05 (kind::tf32)
-// with a 3xTF32 split for FP32-level accuracy.  See cgemm_tc.cu.
+// K2 tensor-core path: complex64 GEMM as a real GEMM on tcgen05.  Default:
+// the CTA-pair kind::f16 kernel with a 3xFP16 split (power-of-two operand
+// scaling, promoted FP32 accumulation) for FP32-level accuracy; 3xTF32
+// (kind::tf32) for shapes the pair kernel does not take or QSG_TC_PREC=tf32.
+// See cgemm_tc.cu.
 #pragma once
 
 #include <cstdint>
