@@ -39,13 +39,14 @@ CONFIGS = {
                       "b_007_003_004 (2 slices), 1024-amplitude batch per x1 draw",
           "slices_per_step": None},
     "3": {"circuit": (11, 12, 32, 0), "mask": 60, "plan": "configs/config3_bristlecone60_plan.json",
-          "workload": "config3: Bristlecone-60 (11x12 diamond embedding) depth (1+32+1), column snake, 10 cut bonds "
-                      "(1024 slices), closed amplitude over the fixed 2^10-slice set; 1 slice per step per GPU",
+          "workload": "config3: Bristlecone-60 (11x12 diamond embedding) depth (1+32+1), clustered column snake, "
+                      "10 cut bonds (K = 1024 slices, max rank 28), closed amplitude over the fixed 2^10-slice set "
+                      "(all of K: full fidelity); 1 slice per step per GPU",
           "slices_per_step": 1, "slices_per_batch": 1024},
     "4": {"circuit": (11, 12, 32, 0), "mask": 70, "plan": "configs/config4_bristlecone70_plan.json",
-          "workload": "config4: Bristlecone-70 (11x12 diamond embedding) depth (1+32+1), column snake, 16 cut bonds "
-                      "(65536 slices, max rank 32), closed amplitude over a fixed 2^12-slice subset; 1 slice per "
-                      "step per GPU",
+          "workload": "config4: Bristlecone-70 (11x12 diamond embedding) depth (1+32+1), clustered column snake, "
+                      "16 cut bonds (K = 65536 slices, max rank 31), closed amplitude over a fixed 2^12-slice "
+                      "subset (path fraction 1/16); 1 slice per step per GPU",
           "slices_per_step": 1, "slices_per_batch": 4096},
     "3s": {"circuit": (6, 10, 32, 0), "plan": "configs/config3_standin_6x10_plan.json",
            "workload": "config3 rectangular stand-in: 6x10 RQC depth (1+32+1), column sweep, 12-bond seam cut "
@@ -567,13 +568,15 @@ def run_ours(args):
     elif top["tensor_cores"]:
         bound, peak_val, peak_note = "tensor", peaks["bf16_tflops"] / 2.0 / 3.0, (
             f"3xTF32 ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 2 (tf32) / 3 (passes)")
-    elif top["bytes"] > 0 and top["flops"] / top["bytes"] < fp32_peak * 1e12 / (peaks["hbm_gbs"] * 1e9):
-        # below the FP32 ridge (11.4 flop/B): the SIMT step is HBM-bound
-        bound, peak_val, peak_note = "hbm", peaks["hbm_gbs"], f"{peak_src} HBM copy bandwidth (GB/s)"
-        achieved = top["bytes"] / (top_ms / 1e3) / 1e9
     else:
         bound, peak_val, peak_note = "tensor", fp32_peak, (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x "
                                                            f"{smx:.0f} MHz ({peak_src} sm_max_mhz)")
+    if top["bytes"] > 0 and top["flops"] / top["bytes"] < peak_val * 1e12 / (peaks["hbm_gbs"] * 1e9):
+        # arithmetic intensity below that ceiling's ridge (e.g. m = 2^28, n = k = 16:
+        # 8 flop/B): the step is HBM-bound whatever pipe it runs on
+        bound, peak_val, peak_note = "hbm", peaks["hbm_gbs"], (
+            f"{peak_src} HBM copy bandwidth (GB/s); algorithmic bytes 8 (mk + kn + mn) of the step")
+        achieved = top["bytes"] / (top_ms / 1e3) / 1e9
     simt_name = "cgemm_narrow" if top["n"] <= 32 and top["m"] >= 1024 else "cgemm_simt"
     kernel_name = (f"cgemm_tc ({split})" if top["tensor_cores"] else simt_name) + \
         f" step s{top['step']:03d} m={top['m']} n={top['n']} k={top['k']}"

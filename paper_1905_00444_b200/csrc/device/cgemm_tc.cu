@@ -133,6 +133,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking probe of an mbarrier phase (true once `parity` completed).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
@@ -1113,46 +1126,68 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       return static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo);
     };
     float local = 0.f;
-    int s = 0;
-    uint32_t ph = 0;
-    for (long long q = 0; q <= total_chunks; ++q) {
-      if (!kSplitA && q < total_chunks) {
-        const int c = static_cast<int>(q % nchunks);
-        const int kb_end = min(kblocks, (c + 1) * p.chunk);
-        for (int kb = c * p.chunk; kb < kb_end; ++kb) {
-          mbar_wait(&full[s], ph);
-          uint8_t* st = smem + s * Cfg::STAGE_BYTES;
-          // In place, warp-local: each 8-row group g of a box (1 KiB of raw
-          // fp32) becomes its hi (512 B) and lo (512 B) SW64 atoms, so A_hi
-          // / A_lo are 8-row atoms at a 1 KiB stride (SBO) and no warp
-          // touches another warp's rows.  Lane = (row rl, 8-column group cg).
-          {
-            const int rl = lane >> 2, cg = lane & 3;
-            const int iters = (p.half_tail && kb == kblocks - 1 ? 1 : 2) * (BM / 8) / (kWorkers / 32);
+    // Raw-A stage conversion, serviced cooperatively: the same warps convert
+    // the stages of chunk q and write the epilogue of chunk q - 1.  Converting
+    // all of chunk q first (each stage gated by the MMA freeing a smem slot)
+    // left the tensor pipe idle during every epilogue (~51% busy on the
+    // k = 256 class); now the epilogue polls between slabs and converts any
+    // stage that has landed, so the MMA of chunk q runs under the epilogue
+    // of chunk q - 1.  Cursor: next (chunk, k-block) to convert.
+    int cv_s = 0;
+    uint32_t cv_ph = 0;
+    long long cv_q = 0;
+    int cv_kb = 0;
+    auto convert_stage = [&](int kb) {
+      uint8_t* st = smem + cv_s * Cfg::STAGE_BYTES;
+      // In place, warp-local: each 8-row group g of a box (1 KiB of raw
+      // fp32) becomes its hi (512 B) and lo (512 B) SW64 atoms, so A_hi
+      // / A_lo are 8-row atoms at a 1 KiB stride (SBO) and no warp
+      // touches another warp's rows.  Lane = (row rl, 8-column group cg).
+      const int rl = lane >> 2, cg = lane & 3;
+      const int iters = (p.half_tail && kb == kblocks - 1 ? 1 : 2) * (BM / 8) / (kWorkers / 32);
 #pragma unroll 1
-            for (int it = 0; it < iters; ++it) {
-              const int gi = it * (kWorkers / 32) + (warp - 2);  // 0..31 over both boxes
-              uint8_t* grp = st + (gi >> 4) * (Cfg::A_B / 2) + (gi & 15) * 1024;
-              const float4 x0 = *reinterpret_cast<const float4*>(grp + rl * 128 + (((2 * cg) ^ rl) << 4));
-              const float4 x1 = *reinterpret_cast<const float4*>(grp + rl * 128 + (((2 * cg + 1) ^ rl) << 4));
-              __syncwarp();
-              uint4 h, l;
-              split_f16x8(x0, x1, scale_a, h, l);
-              const int off = rl * 64 + ((cg ^ ((rl >> 1) & 3)) << 4);
-              *reinterpret_cast<uint4*>(grp + off) = h;
-              *reinterpret_cast<uint4*>(grp + 512 + off) = l;
-            }
-          }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&conv[s]);  // this warp's rows are converted
-          if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+      for (int it = 0; it < iters; ++it) {
+        const int gi = it * (kWorkers / 32) + (warp - 2);  // 0..31 over both boxes
+        uint8_t* grp = st + (gi >> 4) * (Cfg::A_B / 2) + (gi & 15) * 1024;
+        const float4 x0 = *reinterpret_cast<const float4*>(grp + rl * 128 + (((2 * cg) ^ rl) << 4));
+        const float4 x1 = *reinterpret_cast<const float4*>(grp + rl * 128 + (((2 * cg + 1) ^ rl) << 4));
+        __syncwarp();
+        uint4 h, l;
+        split_f16x8(x0, x1, scale_a, h, l);
+        const int off = rl * 64 + ((cg ^ ((rl >> 1) & 3)) << 4);
+        *reinterpret_cast<uint4*>(grp + off) = h;
+        *reinterpret_cast<uint4*>(grp + 512 + off) = l;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[cv_s]);  // this warp's rows are converted
+      if (++cv_s == Cfg::STAGES) { cv_s = 0; cv_ph ^= 1; }
+    };
+    // Convert stages of chunks <= q_lim: all of them (block) or only those
+    // whose TMA has landed (poll).
+    auto service = [&](long long q_lim, bool block) {
+      if constexpr (!kSplitA) {
+        while (cv_q <= q_lim && cv_q < total_chunks) {
+          const int c = static_cast<int>(cv_q % nchunks);
+          const int kb = c * p.chunk + cv_kb;
+          if (block) mbar_wait(&full[cv_s], cv_ph);
+          else if (!__shfl_sync(0xffffffffu, mbar_test(&full[cv_s], cv_ph) ? 1 : 0, 0)) return;  // warp-uniform
+          convert_stage(kb);
+          if (++cv_kb == min(kblocks, (c + 1) * p.chunk) - c * p.chunk) { cv_kb = 0; ++cv_q; }
         }
       }
+    };
+    for (long long q = 0; q <= total_chunks; ++q) {
+      if (q == 0) service(0, true);
       if (q >= 1) {
         const long long qq = q - 1;
         const int buf = static_cast<int>(qq & 1);
-        mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1));
+        if constexpr (kSplitA) {
+          mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1));
+        } else {
+          while (!__shfl_sync(0xffffffffu, mbar_test(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1)) ? 1 : 0, 0))
+            service(q, false);
+        }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if constexpr (!kDirect) {
 #pragma unroll
@@ -1205,6 +1240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               const int sw = (lane >> 2) & 7;  // r & 7 of every row this lane reads
 #pragma unroll
               for (int c0 = 0; c0 < HALF; c0 += 32) {
+                service(q, false);
 #pragma unroll
                 for (int h16 = 0; h16 < 2; ++h16) {
                   float a16[16];
@@ -1268,6 +1304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (!stored) {
 #pragma unroll
           for (int c0 = 0; c0 < HALF; c0 += 16) {
+            if ((c0 & 31) == 0) service(q, false);
             float a16[16];
             if constexpr (kDirect) {
               tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0), a16);
