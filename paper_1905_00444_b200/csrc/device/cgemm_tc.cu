@@ -102,6 +102,8 @@ struct TcParams {
   long long c_total;   // complex elements of C (offset of the lo plane / 4 bytes)
   int stream_store;    // fp16 kernel: evict-first (st.global.cs) output stores
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
+  int passes;         // fp16 kernel: 3 (hi.hi + hi.lo + lo.hi); 2 = power-model experiment only (QSG_TC_PASSES)
+  int convert_ahead;  // fp16 kernel, raw A: convert a chunk's stages before the previous chunk's epilogue (A/B knob)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
   unsigned char col_pos[24];
@@ -1038,7 +1040,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint64_t adv = static_cast<uint64_t>(kk * 32 >> 4);
             umma2_f16_if(leader, d, a_hi, b_hi + adv, idesc, (first && kk == 0) ? 0u : 1u);
             umma2_f16_if(leader, d, a_hi, b_lo + adv, idesc, 1u);
-            umma2_f16_if(leader, d, a_lo, b_hi + adv, idesc, 1u);
+            if (p.passes >= 3) umma2_f16_if(leader, d, a_lo, b_hi + adv, idesc, 1u);
           }
           umma2_commit_both_if(leader, &empty[s]);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
@@ -1178,7 +1180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     };
     for (long long q = 0; q <= total_chunks; ++q) {
-      if (q == 0) service(0, true);
+      if (q == 0 || p.convert_ahead) service(q, true);
       if (q >= 1) {
         const long long qq = q - 1;
         const int buf = static_cast<int>(qq & 1);
@@ -1690,6 +1692,8 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.log2k = l2k;
   p.c_total = g.m * g.n;
   p.stream_store = std::getenv("QSG_TC_STCS") && std::getenv("QSG_TC_STCS")[0] == '0' ? 0 : 1;  // measured ~2% on config 2
+  p.passes = env_int("QSG_TC_PASSES", 3) == 2 ? 2 : 3;  // 2: inaccurate, measures MMA-count vs power only
+  p.convert_ahead = std::getenv("QSG_TC_SERVICE") && std::getenv("QSG_TC_SERVICE")[0] == '0' ? 1 : 0;
   p.meta_a = meta_a;
   p.meta_b = meta_b;
   p.meta_c = g.meta_c;
