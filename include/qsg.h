@@ -277,6 +277,16 @@ int qsg_reassociate_plan(const char* circuit_text, int kind, const char* plan_te
                          char* buf, int64_t cap, int64_t* len, int* rewrites);
 int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
                           const int64_t* slice_ids, int64_t k, double* amps_host, char* bitstrings_host);
+/* Pipelined qsg_amplitude_batches: _submit validates the draws, enqueues the
+ * contraction and the D2H of its batch into pinned staging slot `slot`
+ * (0 or 1) on the engine stream and returns at once; _collect waits for
+ * that slot and writes the per-draw amplitudes (and bitstrings, if non-NULL)
+ * exactly as qsg_amplitude_batches does.  Pass collect the same draw list.
+ * With two slots the host gathers batch i while the GPU runs batch i + 1. */
+int qsg_amplitude_batches_submit(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
+                                 const int64_t* slice_ids, int64_t k, int slot);
+int qsg_amplitude_batches_collect(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
+                                  int slot, double* amps_host, char* bitstrings_host);
 
 /* run_amplitudes (src/engine.cpp:300-378) for closed plans: nb bitstrings
  * of n chars, fraction num/den (den <= 0: all slices), seed.  out: nb

@@ -150,6 +150,8 @@ def lib():
         "qsg_widen_plan": (i32, [cp, i32, cp, P(i32), i32, P(i32), i32, cp, i64, P(i64)]),
         "qsg_reassociate_plan": (i32, [cp, i32, cp, P(i32), i32, cp, i64, P(i64), P(i32)]),
         "qsg_amplitude_batches": (i32, [vp, P(i32), i32, P(i32), i32, i32, P(i64), i64, dp, cp]),
+        "qsg_amplitude_batches_submit": (i32, [vp, P(i32), i32, P(i32), i32, i32, P(i64), i64, i32]),
+        "qsg_amplitude_batches_collect": (i32, [vp, P(i32), i32, P(i32), i32, i32, i32, dp, cp]),
         "qsg_run_amplitudes": (i32, [vp, cp, i32, i32, i64, i64, u64, dp, P(i64), P(u64)]),
         "qsg_sample": (i32, [vp, i64, i64, i64, i32, C.c_double, u64, cp, dp, P(_SampleStats), P(_XebReport)]),
         "qsg_xeb_score": (i32, [i32, dp, i64, i32, C.c_double, P(_XebReport)]),
@@ -585,6 +587,34 @@ class Engine:
         bits = C.create_string_buffer(max(1, n * per * nx1)) if bitstrings else None
         _check(lib().qsg_amplitude_batches(self._h, pb, len(b), _p(xs, C.c_int), nx1, n, _p(ids, C.c_int64), len(ids),
                                            _p(amps, C.c_double), bits))
+        amps = amps.view(np.complex128).reshape(nx1, per)
+        if not bitstrings:
+            return amps
+        raw = bits.raw
+        return [([raw[(t * per + j) * n:(t * per + j + 1) * n].decode() for j in range(per)], amps[t])
+                for t in range(nx1)]
+
+    def amplitude_batches_submit(self, base_open, x1_list, slice_ids, slot: int = 0):
+        """Pipelined amplitude_batches: enqueue the contraction and the D2H of its
+        batch into staging slot 0/1 and return; amplitude_batches_collect(slot)
+        later returns the [draws, 2^|open|] amplitudes (or (bitstrings, amps))."""
+        b, pb = _i32(base_open)
+        xs = np.ascontiguousarray(np.asarray(x1_list, dtype=np.int32))
+        nx1, n = xs.shape
+        ids = np.ascontiguousarray(np.asarray(list(slice_ids), dtype=np.int64))
+        _check(lib().qsg_amplitude_batches_submit(self._h, pb, len(b), _p(xs, C.c_int), nx1, n, _p(ids, C.c_int64),
+                                                  len(ids), slot))
+        self._pending = getattr(self, "_pending", {})
+        self._pending[slot] = (b, xs)
+
+    def amplitude_batches_collect(self, slot: int = 0, bitstrings: bool = False):
+        b, xs = self._pending.pop(slot)
+        nx1, n = xs.shape
+        per = 1 << len(b)
+        amps = np.empty(2 * per * nx1, dtype=np.float64)
+        bits = C.create_string_buffer(max(1, n * per * nx1)) if bitstrings else None
+        _check(lib().qsg_amplitude_batches_collect(self._h, _p(b, C.c_int), len(b), _p(xs, C.c_int), nx1, n, slot,
+                                                   _p(amps, C.c_double), bits))
         amps = amps.view(np.complex128).reshape(nx1, per)
         if not bitstrings:
             return amps

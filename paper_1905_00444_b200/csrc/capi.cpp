@@ -665,6 +665,27 @@ int qsg_amplitude_batches(qsg_engine* e, const int* base_open, int nbase, const 
   });
 }
 
+int qsg_amplitude_batches_submit(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
+                                 const int64_t* slice_ids, int64_t k, int slot) {
+  return guarded([&] {
+    if (nx1 < 0) throw std::invalid_argument("amplitude_batches: negative draw count");
+    if (n != e->impl->circuit().num_qubits()) throw std::invalid_argument("fold: bitstring length != qubit count");
+    qsg::amplitude_batches_submit(*e->impl, std::vector<int>(base_open, base_open + nbase), x1_list,
+                                  static_cast<std::size_t>(nx1), std::vector<std::int64_t>(slice_ids, slice_ids + k),
+                                  slot);
+  });
+}
+
+int qsg_amplitude_batches_collect(qsg_engine* e, const int* base_open, int nbase, const int* x1_list, int nx1, int n,
+                                  int slot, double* amps_out, char* bits_out) {
+  return guarded([&] {
+    if (nx1 < 0) throw std::invalid_argument("amplitude_batches: negative draw count");
+    if (n != e->impl->circuit().num_qubits()) throw std::invalid_argument("fold: bitstring length != qubit count");
+    qsg::amplitude_batches_collect(*e->impl, std::vector<int>(base_open, base_open + nbase), x1_list,
+                                   static_cast<std::size_t>(nx1), slot, amps_out, bits_out);
+  });
+}
+
 int qsg_run_amplitudes(qsg_engine* e, const char* bitstrings, int nb, int n, int64_t frac_num, int64_t frac_den,
                        uint64_t seed, double* out, int64_t* ids_out, uint64_t* flops) {
   return guarded([&] {

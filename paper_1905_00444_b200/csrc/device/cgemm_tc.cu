@@ -221,6 +221,17 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16 columns TMEM -> registers without the trailing wait (issue several,
+// then one tcgen05.wait::ld before reading any of them).
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr));
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     cgemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_bhi,
@@ -869,7 +880,7 @@ struct Tc5Cfg {
 // accumulator buffer after the tile's stores (the MMA meanwhile fills the
 // other buffer).  Without the 128 promoted floats per thread the worker
 // warps run spill-free.
-template <int kPairBN, bool kSplitA, int kBK = BK16, bool kDirect = false>
+template <int kPairBN, bool kSplitA, int kBK = BK16, int kDirect = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_alo,
                           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -1077,9 +1088,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    float acc[kDirect ? 1 : HALF];
+    float acc[kDirect == 1 ? 1 : HALF];
 #pragma unroll
-    for (int i = 0; i < (kDirect ? 1 : HALF); ++i) acc[i] = 0.f;
+    for (int i = 0; i < (kDirect == 1 ? 1 : HALF); ++i) acc[i] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
     const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
     const int ea = p.a_presplit ? p.meta_a->split_exp : f16_exp(p.meta_a), eb = f16_exp(p.meta_b);
@@ -1202,6 +1213,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        } else if constexpr (kDirect == 2) {
+          // Early release: the whole accumulator slice goes to registers in
+          // one burst of TMEM loads (one wait), and the buffer is handed
+          // back to the MMA before any conversion or store.  With two 256-
+          // column buffers the MMA otherwise waits for the slab-by-slab
+          // epilogue of tile t before it may start tile t + 2.
+#pragma unroll
+          for (int j = 0; j < HALF / 16; ++j)
+            tmem_ld16_nowait(lane_base + static_cast<uint32_t>(buf * kPairBN + 16 * j), &acc[16 * j]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
         if (kDirect || qq % nchunks == nchunks - 1) {
           long long m_pair;
@@ -1246,7 +1270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int h16 = 0; h16 < 2; ++h16) {
                   float a16[16];
-                  if constexpr (kDirect) {
+                  if constexpr (kDirect == 1) {
                     tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0 + 16 * h16), a16);
                   } else {
 #pragma unroll
@@ -1308,7 +1332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int c0 = 0; c0 < HALF; c0 += 16) {
             if ((c0 & 31) == 0) service(q, false);
             float a16[16];
-            if constexpr (kDirect) {
+            if constexpr (kDirect == 1) {
               tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0), a16);
             } else {
 #pragma unroll
@@ -1377,10 +1401,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             __syncwarp();
           }
           }
-          if constexpr (kDirect) {
+          if constexpr (kDirect == 1) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
-          } else {
+          } else if constexpr (kDirect == 0) {
 #pragma unroll
             for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
           }
@@ -1726,9 +1750,13 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
     return resident_pairs(cgemm_f16_pair_kernel<BN, false>, Tc5Cfg<BN>::SMEM);
   }();
   static const bool attrs_direct = [] {
-    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Tc5Cfg<BN>::SMEM);
-    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tc5Cfg<BN>::SMEM);
+    cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Tc5Cfg<BN>::SMEM);
     return true;
   }();
@@ -1736,10 +1764,16 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   const long long clusters = std::min<long long>(pairs, slots);
   const unsigned grid = static_cast<unsigned>(2 * clusters);
   const bool direct = p.kblocks <= p.chunk && !(std::getenv("QSG_TC_DIRECT") && std::getenv("QSG_TC_DIRECT")[0] == '0');
-  if (direct && split)
-    cgemm_f16_pair_kernel<BN, true, BK16, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  // Early TMEM release for single-chunk tiles (QSG_TC_EARLY=0: slab-by-slab reads).
+  static const bool early = std::getenv("QSG_TC_EARLY") && std::getenv("QSG_TC_EARLY")[0] == '1';
+  if (direct && split && early)
+    cgemm_f16_pair_kernel<BN, true, BK16, 2><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  else if (direct && early)
+    cgemm_f16_pair_kernel<BN, false, BK16, 2><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+  else if (direct && split)
+    cgemm_f16_pair_kernel<BN, true, BK16, 1><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else if (direct)
-    cgemm_f16_pair_kernel<BN, false, BK16, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    cgemm_f16_pair_kernel<BN, false, BK16, 1><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else if (split)
     cgemm_f16_pair_kernel<BN, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else

@@ -176,6 +176,10 @@ Engine::~Engine() {
   if (metas_) cudaFree(metas_);
   if (acc_) cudaFree(acc_);
   if (acc_host_) cudaFreeHost(acc_host_);
+  for (auto& st : stage_) {
+    if (st.host) cudaFreeHost(st.host);
+    if (st.ev) cudaEventDestroy(st.ev);
+  }
   if (per_slice_) cudaFree(per_slice_);
   if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -1029,6 +1033,25 @@ const cdouble* Engine::results_pinned() {
   return reinterpret_cast<const cdouble*>(acc_host_);
 }
 
+void Engine::stage_results(int slot) {
+  if (slot < 0 || slot > 1) throw std::out_of_range("stage_results: slot must be 0 or 1");
+  check(cudaSetDevice(opt_.device), "cudaSetDevice");
+  const std::size_t acc_bytes = sizeof(double2) * static_cast<std::size_t>(batch_);
+  auto& st = stage_[static_cast<std::size_t>(slot)];
+  if (!st.host) check(cudaMallocHost(&st.host, acc_bytes), "pinned staging");
+  if (!st.ev) check(cudaEventCreateWithFlags(&st.ev, cudaEventDisableTiming), "event");
+  check(cudaMemcpyAsync(st.host, acc_, acc_bytes, cudaMemcpyDeviceToHost, stream_), "result copy");
+  check(cudaEventRecord(st.ev, stream_), "event record");
+}
+
+const cdouble* Engine::staged_results(int slot) {
+  if (slot < 0 || slot > 1 || !stage_[static_cast<std::size_t>(slot)].ev)
+    throw std::invalid_argument("staged_results: nothing staged in this slot");
+  auto& st = stage_[static_cast<std::size_t>(slot)];
+  check(cudaEventSynchronize(st.ev), "staged result sync");
+  return reinterpret_cast<const cdouble*>(st.host);
+}
+
 void Engine::synchronize() {
   check(cudaSetDevice(opt_.device), "cudaSetDevice");
   check(cudaStreamSynchronize(stream_), "sync");
@@ -1114,8 +1137,10 @@ ContractionPlan widen_plan(const Circuit& c, const ContractionPlan& plan, const 
   return p;
 }
 
-void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
-                            const std::vector<std::int64_t>& slice_ids, double* amps_out, char* bits_out) {
+namespace {
+// Validates a draw list against the widened plan; returns the widened x1.
+std::vector<int> widened_x1(const Engine& wide, const std::vector<int>& base_open, const int* x1_list,
+                            std::size_t nx1) {
   const int n = wide.circuit().num_qubits();
   const auto& wopen = wide.plan().open_qubits;
   std::vector<char> is_open(static_cast<std::size_t>(n), 0), is_base(static_cast<std::size_t>(n), 0);
@@ -1127,10 +1152,10 @@ void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, con
       throw std::invalid_argument("amplitude_batches: base open qubits must be open in the widened plan");
     is_base[static_cast<std::size_t>(q)] = 1;
   }
-  if (nx1 == 0) return;
   auto draw = [&](std::size_t t) { return x1_list + t * static_cast<std::size_t>(n); };
   // One contraction: the widened plan's closed qubits must agree across the list.
   std::vector<int> x1w(static_cast<std::size_t>(n), -1);
+  if (nx1 == 0) return x1w;
   for (int q = 0; q < n; ++q)
     if (!is_open[static_cast<std::size_t>(q)]) x1w[static_cast<std::size_t>(q)] = draw(0)[q];
   for (std::size_t t = 0; t < nx1; ++t) {
@@ -1144,9 +1169,26 @@ void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, con
         throw std::invalid_argument("amplitude_batches: x1 draws differ on a qubit the widened plan keeps closed");
     }
   }
+  return x1w;
+}
+}  // namespace
+
+void amplitude_batches_submit(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                              const std::vector<std::int64_t>& slice_ids, int slot) {
+  const std::vector<int> x1w = widened_x1(wide, base_open, x1_list, nx1);
+  if (nx1 == 0) return;
   wide.prepare(x1w);
   wide.run(slice_ids, /*reset=*/true, /*per_slice=*/false);
-  const cdouble* amps = wide.results_pinned();
+  wide.stage_results(slot);
+}
+
+void amplitude_batches_collect(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                               int slot, double* amps_out, char* bits_out) {
+  if (nx1 == 0) return;
+  const int n = wide.circuit().num_qubits();
+  const auto& wopen = wide.plan().open_qubits;
+  auto draw = [&](std::size_t t) { return x1_list + t * static_cast<std::size_t>(n); };
+  const cdouble* amps = wide.staged_results(slot);
   // Batch index of a full bitstring: bit (|open|-1-r) <-> r-th smallest open qubit (src/sampler.cpp:41-52).
   // wide index = fixed part (this draw's bits on the extra open qubits) + the
   // base batch index's bits scattered to the base qubits' positions.
@@ -1189,6 +1231,12 @@ void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, con
       }
     }
   }
+}
+
+void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                            const std::vector<std::int64_t>& slice_ids, double* amps_out, char* bits_out) {
+  amplitude_batches_submit(wide, base_open, x1_list, nx1, slice_ids, 0);
+  amplitude_batches_collect(wide, base_open, x1_list, nx1, 0, amps_out, bits_out);
 }
 
 std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(

@@ -112,6 +112,11 @@ class Engine {
   // The batch in the engine's pinned staging buffer (synchronises; valid
   // until the next results call): no allocation on the hot path.
   const cdouble* results_pinned();
+  // Asynchronous result staging (two slots): D2H of the batch accumulator
+  // into a pinned slot + event, enqueued after the current run; the host
+  // collects it later, so it can prepare the next batch meanwhile.
+  void stage_results(int slot);
+  const cdouble* staged_results(int slot);  // waits for that slot's copy
   void synchronize();
 
   std::int64_t launches() const { return launches_; }
@@ -216,6 +221,11 @@ class Engine {
   int nmeta_ = 0;
   double2* acc_ = nullptr;
   double2* acc_host_ = nullptr;  // pinned staging of the batch for results()
+  struct Stage {
+    double2* host = nullptr;
+    cudaEvent_t ev = nullptr;
+  };
+  Stage stage_[2];
   double2* per_slice_ = nullptr;
   std::int64_t per_slice_cap_ = 0;
   std::int64_t per_slice_used_ = 0;
@@ -260,6 +270,14 @@ std::vector<std::vector<std::pair<std::string, cdouble>>> amplitude_batches(
     const std::vector<std::int64_t>& slice_ids, bool with_bitstrings = true);
 // Same, flat buffers: x1_list nx1 x n ints; writes nx1 x 2^|base| (re, im)
 // and, if bits_out, the bitstrings (n chars each) in the same order.
+// Pipelined form of amplitude_batches_into: submit enqueues the contraction
+// and the D2H of its batch into staging slot `slot` (0/1) and returns;
+// collect waits for that slot and gathers the per-draw amplitudes.  The
+// draw list passed to collect must be the one given to submit.
+void amplitude_batches_submit(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                              const std::vector<std::int64_t>& slice_ids, int slot);
+void amplitude_batches_collect(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
+                               int slot, double* amps_out, char* bits_out);
 void amplitude_batches_into(Engine& wide, const std::vector<int>& base_open, const int* x1_list, std::size_t nx1,
                             const std::vector<std::int64_t>& slice_ids, double* amps_out, char* bits_out);
 

@@ -17,7 +17,13 @@ def main():
     rs = [r for r in rows(path) if r["Metric Name"] == "gpu__time_duration.sum"]
     hits = [(i, float(r["Metric Value"])) for i, r in enumerate(x for x in rs if name in x["Kernel Name"])]
     rng = [float(a.split("=")[1]) * 1e6 for a in sys.argv if a.startswith("--ms=")]  # --ms=LO --ms=HI (ms)
-    if len(rng) == 2:
+    variant = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    if variant:  # index among all `name` launches (ncu -k regex:name -s IDX), longest of one template variant
+        names = [x["Kernel Name"] for x in rs if name in x["Kernel Name"]]
+        cand = [(i, v) for i, v in hits if variant[0] in names[i]]
+        top = max(v for _, v in cand)
+        print(min(i for i, v in cand if v >= 0.95 * top))
+    elif len(rng) == 2:
         print(min(i for i, v in hits if rng[0] <= v <= rng[1]))  # first launch in the duration window
     else:
         top = max(v for _, v in hits)

@@ -313,6 +313,14 @@ def test_amplitude_batches_widened_plan(gpu):
     draws = [gpu.draw_x1(16, base, 0, i) for i in range(64)]
     with gpu.Engine(text, wide) as e:
         got = e.amplitude_batches(base, draws, [0])
+        # pipelined form: two batches in flight, collected in order, bit-identical
+        halves = [draws[:32], draws[32:]]
+        e.amplitude_batches_submit(base, halves[0], [0], slot=0)
+        e.amplitude_batches_submit(base, halves[1], [0], slot=1)
+        late = e.amplitude_batches_collect(1, bitstrings=True)
+        early = e.amplitude_batches_collect(0, bitstrings=True)
+        for (b1, a1), (b2, a2) in zip(early + late, got):
+            assert b1 == b2 and np.array_equal(a1, a2)
     with gpu.Engine(text, plan) as e:
         for x1, (bits, amps) in zip(draws[:8], got[:8]):
             rbits, ramps = e.amplitude_batch(x1, [0])
