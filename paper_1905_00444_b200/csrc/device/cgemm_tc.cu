@@ -1796,6 +1796,208 @@ void setup_attr() {
   });
 }
 
+
+// ---------------------------------------------------------------------------
+// 3M (Gauss / Karatsuba) complex products on the same CTA-pair kernel.
+//   P1 = Ar Br,  P2 = Ai Bi,  P3 = (Ar + Ai)(Br + Bi)
+//   Re C = P1 - P2,  Im C = P3 - P1 - P2
+// three REAL GEMMs of the complex shape (3 m n k MACs) instead of the 2x2
+// embedding's one real GEMM of 4 m n k MACs: 25% fewer tensor-core passes,
+// which under the board's power cap is the lever left (measured: dropping a
+// third of the MMAs ran config 2 / 5 1.22-1.26x faster).  Each real product
+// is the pair kernel on a "complex" shape (m, n/2, k/2): A = the [m][k] real
+// plane pair, B^T = the [n][k] real plane pair, C = [m][n] fp32.  Operand
+// planes are built by one streaming pass each (A: 20 B per complex element,
+// B: small), the products go to workspace, and a combine pass forms C,
+// applies the operands' pending renormalisation and updates TMeta.  Used on
+// compute-heavy steps only (n, k >= kMin3M): the operand passes cost ~300/n
+// and the combine ~480/k of the GEMM's time, and the step loses the fused
+// store / split hand-offs (the combine writes complex64 in natural order).
+// Measured: config 5's 2^15 cubes 1007 -> 839 ms, config 2 506 -> 403 ms per
+// batch; at n = k = 1024 (config 5's 2^20 x 2^10 x 2^10 steps) it lost 35%.
+constexpr std::int64_t kMin3M = 4096;
+
+// |S| = |Re + Im| <= sqrt(2) max|z|: one exponent below the 2x2 path's.
+__device__ __forceinline__ int f16_exp_3m(const TMeta* m) { return f16_exp(m) - 1; }
+
+__device__ __forceinline__ void split16(float x, __half& hi, __half& lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(x - __half2float(hi));
+}
+
+// A (complex [m][k]: raw fp32, or split fp16 hi | lo planes of the 2x2 path
+// with value (hi + lo) 2^-split_exp) -> Ar, Ai, S = Ar + Ai, each as fp16
+// hi | lo planes [m][k] scaled by 2^(f16_exp(meta) - 1).
+__global__ void __launch_bounds__(256) tc3m_prep_a_kernel(const void* __restrict__ a, int presplit,
+                                                          long long count, const TMeta* __restrict__ meta,
+                                                          __half* __restrict__ planes, TMeta* __restrict__ scratch) {
+  const int ea = f16_exp_3m(meta);
+  const float s = scalbnf(1.f, ea - (presplit ? meta->split_exp : 0));
+  if (blockIdx.x == 0 && threadIdx.x == 0) scratch->split_exp = ea;
+  __half* const arh = planes;
+  __half* const arl = arh + count;
+  __half* const aih = arl + count;
+  __half* const ail = aih + count;
+  __half* const ssh = ail + count;
+  __half* const ssl = ssh + count;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < count; i += static_cast<long long>(gridDim.x) * 256) {
+    float re, im;
+    if (presplit) {
+      const __half2 h = reinterpret_cast<const __half2*>(a)[i];
+      const __half2 l = reinterpret_cast<const __half2*>(a)[count + i];
+      re = __low2float(h) + __low2float(l);
+      im = __high2float(h) + __high2float(l);
+    } else {
+      const float2 v = reinterpret_cast<const float2*>(a)[i];
+      re = v.x;
+      im = v.y;
+    }
+    re *= s;
+    im *= s;
+    split16(re, arh[i], arl[i]);
+    split16(im, aih[i], ail[i]);
+    split16(re + im, ssh[i], ssl[i]);
+  }
+}
+
+// B (complex [k][n], or [n][k] when tb) -> B^T real planes [n][k]: Br, Bi,
+// T = Br + Bi, each fp16 hi | lo scaled by 2^(f16_exp(meta) - 1).
+__global__ void __launch_bounds__(256) tc3m_prep_b_kernel(const float2* __restrict__ b, long long n, long long k,
+                                                          int tb, const TMeta* __restrict__ meta,
+                                                          __half* __restrict__ planes) {
+  __shared__ float2 tile[32][33];
+  const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 32; r += 8) {
+    if (!tb) {
+      const long long p = p0 + r, j = j0 + tx;
+      tile[r][tx] = (p < k && j < n) ? b[p * n + j] : make_float2(0.f, 0.f);
+    } else {
+      const long long j = j0 + r, p = p0 + tx;
+      tile[tx][r] = (p < k && j < n) ? b[j * k + p] : make_float2(0.f, 0.f);
+    }
+  }
+  __syncthreads();
+  const float s = scalbnf(1.f, f16_exp_3m(meta));
+  const long long nk = n * k;
+  for (int r = ty; r < 32; r += 8) {
+    const long long j = j0 + r, p = p0 + tx;
+    if (j >= n || p >= k) continue;
+    const float2 v = tile[tx][r];
+    const long long o = j * k + p;
+    split16(v.x * s, planes[o], planes[nk + o]);
+    split16(v.y * s, planes[2 * nk + o], planes[3 * nk + o]);
+    split16((v.x + v.y) * s, planes[4 * nk + o], planes[5 * nk + o]);
+  }
+}
+
+// C = (P1 - P2) + i (P3 - P1 - P2), times the operands' pending power-of-two
+// renormalisation; max |c|^2 -> meta_c, log_scale as the pair epilogue sets it.
+__global__ void __launch_bounds__(256) tc3m_combine_kernel(const float4* __restrict__ p1, const float4* __restrict__ p2,
+                                                           const float4* __restrict__ p3, float4* __restrict__ c,
+                                                           long long n4, const TMeta* meta_a, const TMeta* meta_b,
+                                                           int norm_a, int norm_b, TMeta* meta_c) {
+  const int shift = tc_pending_shift(meta_a, norm_a) + tc_pending_shift(meta_b, norm_b);
+  const float f = scalbnf(1.f, -shift);
+  float local = 0.f;
+  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < n4; i += static_cast<long long>(gridDim.x) * 256) {
+    const float4 a = p1[i], b = p2[i], d = p3[i];
+    const float4 lo = make_float4((a.x - b.x) * f, (d.x - a.x - b.x) * f, (a.y - b.y) * f, (d.y - a.y - b.y) * f);
+    const float4 hi = make_float4((a.z - b.z) * f, (d.z - a.z - b.z) * f, (a.w - b.w) * f, (d.w - a.w - b.w) * f);
+    c[2 * i] = lo;
+    c[2 * i + 1] = hi;
+    local = fmaxf(local, fmaxf(fmaxf(lo.x * lo.x + lo.y * lo.y, lo.z * lo.z + lo.w * lo.w),
+                               fmaxf(hi.x * hi.x + hi.y * hi.y, hi.z * hi.z + hi.w * hi.w)));
+  }
+  if (meta_c) {
+    for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
+    if ((threadIdx.x & 31) == 0 && local > 0.f) atomicMax(&meta_c->maxsq_bits, __float_as_uint(local));
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      meta_c->log_scale = (meta_a ? meta_a->log_scale : 0.0) + (meta_b ? meta_b->log_scale : 0.0) + shift;
+  }
+}
+
+// B scratch meta: max |z| doubled (max |z|^2 x 4), so f16_exp(meta_b3) is
+// the exponent the 3M B planes were scaled with.
+__global__ void tc3m_scale_meta_kernel(TMeta* m) {
+  const unsigned bits = m->maxsq_bits;
+  if (bits != 0 && bits < 0x7f800000u) m->maxsq_bits = __float_as_uint(__uint_as_float(bits) * 4.f);
+}
+
+bool use_3m(std::int64_t m, std::int64_t n, std::int64_t k) {
+  const char* env = std::getenv("QSG_TC_3M");  // 0: the 2x2 embedding everywhere
+  const bool on = !(env && env[0] == '0');
+  return on && n >= kMin3M && k >= kMin3M && n % 2 == 0 && k % 2 == 0 && use_f16(m, n / 2, k / 2) &&
+         (k % BK16) == 0;
+}
+
+// Workspace: [metas | sync | A planes 12 m k | B planes 12 n k | P1 P2 P3 12 m n] bytes.
+std::int64_t ws3m_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
+  return kF16Scratch + sync_bytes(m, n / 2, k / 2) + 12 * m * k + 12 * n * k + 12 * m * n;
+}
+
+cudaError_t cgemm_tc_3m(const GemmArgs& g, const TMeta* ma, const TMeta* mb, cudaStream_t stream, int* launches) {
+  char* ws = static_cast<char*>(g.workspace);
+  TMeta* metas = reinterpret_cast<TMeta*>(ws);  // [2] scan scratch (caller), [3] A, [4] B, [5] C scratch
+  TMeta* meta_a3 = metas + 3;
+  TMeta* meta_b3 = metas + 4;
+  TMeta* meta_c3 = metas + 5;
+  const std::int64_t sb = sync_bytes(g.m, g.n / 2, g.k / 2);
+  unsigned int* sync = sb > 0 ? reinterpret_cast<unsigned int*>(ws + kF16Scratch) : nullptr;
+  __half* ap = reinterpret_cast<__half*>(ws + kF16Scratch + sb);
+  __half* bp = ap + 6 * g.m * g.k;
+  float* pp = reinterpret_cast<float*>(bp + 6 * g.n * g.k);
+  const long long mk = g.m * g.k, nk = g.n * g.k, mn = g.m * g.n;
+  // B's scratch meta: max |z|^2 x 4 so that f16_exp gives the planes' exponent (f16_exp - 1).
+  cudaError_t e = cudaMemcpyAsync(meta_b3, mb, sizeof(TMeta), cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) return e;
+  {
+    const int blocks = static_cast<int>(std::min<long long>((mk + 255) / 256, 148 * 16));
+    tc3m_prep_a_kernel<<<blocks, 256, 0, stream>>>(g.a, g.a_presplit ? 1 : 0, mk, ma, ap, meta_a3);
+    dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
+    tc3m_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), g.n, g.k, g.trans_b ? 1 : 0, mb, bp);
+    tc3m_scale_meta_kernel<<<1, 1, 0, stream>>>(meta_b3);
+    if (launches) *launches += 3;
+  }
+  GemmArgs r{};
+  r.m = g.m;
+  r.n = g.n / 2;  // real [m][n] output = "complex" [m][n/2]
+  r.k = g.k / 2;  // real K = k
+  r.a_presplit = true;
+  r.meta_a = meta_a3;
+  r.meta_b = meta_b3;
+  r.meta_c = meta_c3;
+  r.norm_a = r.norm_b = false;
+  for (int t = 0; t < 3; ++t) {
+    r.a = ap + 2 * t * mk;
+    r.c = pp + t * mn;
+    const __half* bhi = bp + 2 * t * nk;
+    const __half* blo = bhi + nk;
+    if (sync) {
+      e = cudaMemsetAsync(sync, 0, static_cast<size_t>(sb), stream);
+      if (e != cudaSuccess) return e;
+    }
+    const __half* ahi = static_cast<const __half*>(r.a);
+    const __half* alo = ahi + mk;
+    switch (pair_bn(r.n)) {
+      case 256: e = launch_f16_pair<256>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
+      case 128: e = launch_f16_pair<128>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
+      case 64: e = launch_f16_pair<64>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
+      default: e = launch_f16_pair<32>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
+    }
+    if (e != cudaSuccess) return e;
+    if (launches) ++*launches;
+  }
+  const long long n4 = mn / 4;
+  const int blocks = static_cast<int>(std::min<long long>((n4 + 255) / 256, 148 * 16));
+  tc3m_combine_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const float4*>(pp),
+                                                  reinterpret_cast<const float4*>(pp + mn),
+                                                  reinterpret_cast<const float4*>(pp + 2 * mn),
+                                                  static_cast<float4*>(g.c), n4, g.meta_a, g.meta_b,
+                                                  g.norm_a && g.meta_a ? 1 : 0, g.norm_b && g.meta_b ? 1 : 0, g.meta_c);
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
 }  // namespace
 
 bool tc_enabled() {
@@ -1819,15 +2021,16 @@ bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool tran
 }
 
 bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
-  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n);
+  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n) && !use_3m(m, n, k);
 }
 
 bool cgemm_tc_split_ok(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
   // Any fp16 pair shape (a half k-block tail reads zero-filled plane columns it never multiplies).
-  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n);
+  return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n) && !use_3m(m, n, k);
 }
 
 std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k, bool, bool, bool a_presplit) {
+  if (use_3m(m, n, k)) return ws3m_bytes(m, n, k);
   if (a_presplit || use_f16(m, n, k))  // operand maxima + K-sync counters + fp16 B_r^T hi + lo (+ pre-split A)
     return kF16Scratch + sync_bytes(m, n, k) + 2 * (2 * n) * b16_pitch(k) * 2 +
            (!a_presplit && split_a(m, n, k) ? 8 * m * k : 0);
@@ -1835,6 +2038,7 @@ std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64
 }
 
 double cgemm_tc_rate(std::int64_t m, std::int64_t n, std::int64_t k) {
+  if (use_3m(m, n, k)) return 5.5e14;   // 3 real products instead of the 4-MAC embedding
   if (split_a(m, n, k)) return 4.5e14;  // measured 450-630 TF/s (config 2 s026 / config 5 cubes)
   if (use_f16(m, n, k)) return 3.5e14;  // in-kernel A conversion: ~68% tensor-pipe occupancy
   return 1.5e14;                        // 3xTF32
@@ -1842,6 +2046,9 @@ double cgemm_tc_rate(std::int64_t m, std::int64_t n, std::int64_t k) {
 
 double cgemm_tc_prep_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   const double nb = static_cast<double>(n) * static_cast<double>(k);  // complex elements of B
+  if (use_3m(m, n, k))  // A planes, B planes, three fp32 products written + read, C written
+    return 20.0 * static_cast<double>(m) * static_cast<double>(k) + 32.0 * nb +
+           32.0 * static_cast<double>(m) * static_cast<double>(n);
   if (!use_f16(m, n, k)) return 40.0 * nb;                            // read 8, write 32 (fp32 hi + lo)
   return 24.0 * nb + (split_a(m, n, k) ? 16.0 * static_cast<double>(m) * static_cast<double>(k) : 0.0);
 }
@@ -1877,6 +2084,10 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
       cudaError_t e = max_abs_sq(g.b, g.n * g.k, scratch + 1, stream, launches);
       if (e != cudaSuccess) return e;
       mb = scratch + 1;
+    }
+    if (use_3m(g.m, g.n, g.k)) {
+      if (g.store_perm || g.c_split) throw std::invalid_argument("cgemm_tc: the 3M path writes natural-order complex64");
+      return cgemm_tc_3m(g, ma, mb, stream, launches);
     }
     const std::int64_t sb = sync_bytes(g.m, g.n, g.k);
     unsigned int* sync = sb > 0 ? reinterpret_cast<unsigned int*>(static_cast<char*>(g.workspace) + kF16Scratch) : nullptr;

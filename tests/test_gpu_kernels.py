@@ -212,3 +212,29 @@ def test_accumulate_kernel_matches_fp64(gpu):
     want = fin.cpu().to(torch.complex128) * 2.0 ** -3
     assert torch.equal(per.cpu(), want)
     assert torch.equal(acc.cpu(), want + 1)
+
+
+@pytest.mark.parametrize("m,n,k,tb", [(512, 4096, 4096, 0), (256, 4096, 8192, 1), (1024, 8192, 4096, 0)])
+def test_cgemm_tensor_core_3m_matches_fp64_and_embedding(gpu, monkeypatch, m, n, k, tb):
+    """3M (Gauss) complex products on the tensor-core path (n, k >= 4096):
+    P1 = Ar Br, P2 = Ai Bi, P3 = (Ar + Ai)(Br + Bi) as three 3xFP16 real
+    GEMMs + a combine pass.  FP32-level accuracy vs fp64 (1e-5 relative
+    Frobenius, the reference's TTGT tolerance) and agreement with the 2x2
+    embedding path (QSG_TC_3M=0)."""
+    import torch
+    g = torch.Generator().manual_seed(m + n + k)
+    A = torch.complex(torch.rand(m, k, generator=g) - 0.5, torch.rand(m, k, generator=g) - 0.5)
+    B = torch.complex(torch.rand(k, n, generator=g) - 0.5, torch.rand(k, n, generator=g) - 0.5)
+    want = A.to(torch.complex128) @ B.to(torch.complex128)
+    dA = A.cuda()
+    dB = (B.t().contiguous() if tb else B).cuda()
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("QSG_TC_3M", mode)
+        dC = torch.zeros(m, n, dtype=torch.complex64, device="cuda")
+        tc_gemm(gpu, dA.data_ptr(), dB.data_ptr(), dC.data_ptr(), m, n, k, tb)
+        out[mode] = dC.cpu().to(torch.complex128)
+    for mode, got in out.items():
+        err = float((got - want).abs().norm() / want.abs().norm())
+        assert err < 1e-5, (mode, err)
+    assert float((out["1"] - out["0"]).abs().norm() / want.abs().norm()) < 1e-5
