@@ -89,13 +89,26 @@ def idle_qubits(cfg):
 
 
 def tc_split(step):
-    """Operand split the tcgen05 path uses for a GEMM step (mirrors use_f16 in
-    csrc/device/cgemm_tc.cu): 3xFP16 on the CTA-pair kernel when 2k % 64 == 0."""
+    """Operand split the tcgen05 path uses for a GEMM step (mirrors use_f16 /
+    use_3m in csrc/device/cgemm_tc.cu): 3xFP16 on the CTA-pair kernel when
+    2k % 64 == 0, as 3M (three real products) when n, k >= 4096."""
     if os.environ.get("QSG_TC_PREC") == "tf32":
         return "3xTF32"
     n2 = 2 * step["n"]
     pair = step["m"] % 256 == 0 and any(n2 % bn == 0 for bn in (256, 128, 64, 32))
-    return "3xFP16" if pair and (2 * step["k"]) % 32 == 0 else "3xTF32"
+    if not (pair and (2 * step["k"]) % 32 == 0):
+        return "3xTF32"
+    if os.environ.get("QSG_TC_3M", "1") != "0" and step["n"] >= 4096 and step["k"] >= 4096 and step["k"] % 64 == 0:
+        return "3M-3xFP16"
+    return "3xFP16"
+
+
+def tc_ceiling(split, bf16):
+    """Eq.(1)-equivalent ceiling of a tensor-core GEMM path from the bf16 dense
+    rate (f16 = bf16 rate): per complex MAC (8 Eq.1 flop) the 2x2 embedding
+    runs 4 real MACs x 3 passes, 3M 3 real MACs x 3 passes, 3xTF32 the
+    embedding at half rate."""
+    return {"3xFP16": bf16 / 3.0, "3M-3xFP16": bf16 * 4.0 / 9.0, "3xTF32": bf16 / 6.0}[split]
 
 
 def measured_traffic(kernel_name):
@@ -592,13 +605,11 @@ def run_ours(args):
     smx = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * smx * 1e6 / 1e12
     split = tc_split(top)
-    if top["tensor_cores"] and split == "3xFP16":
-        # Eq.1-equivalent ceiling of the 3-pass fp16 split (f16 rate = bf16 rate)
-        bound, peak_val, peak_note = "tensor", peaks["bf16_tflops"] / 3.0, (
-            f"3xFP16 ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 3 (passes)")
-    elif top["tensor_cores"]:
-        bound, peak_val, peak_note = "tensor", peaks["bf16_tflops"] / 2.0 / 3.0, (
-            f"3xTF32 ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s / 2 (tf32) / 3 (passes)")
+    if top["tensor_cores"]:
+        how = {"3xFP16": "/ 3 (passes)", "3M-3xFP16": "x 4/9 (3M: 3 real products x 3 passes per 4 MACs)",
+               "3xTF32": "/ 2 (tf32) / 3 (passes)"}[split]
+        bound, peak_val, peak_note = "tensor", tc_ceiling(split, peaks["bf16_tflops"]), (
+            f"{split} ceiling = {peak_src} bf16 dense {peaks['bf16_tflops']} TF/s {how}")
     else:
         bound, peak_val, peak_note = "tensor", fp32_peak, (f"FP32 FFMA peak 148 SM x 128 lanes x 2 x "
                                                            f"{smx:.0f} MHz ({peak_src} sm_max_mhz)")
@@ -634,7 +645,7 @@ def run_ours(args):
 
     tc_share = sum(p["ms_total"] for p in gemms if p["tensor_cores"]) / max(total_ms, 1e-30)
     if tc_share > 0.5:
-        dtype_label = (f"c64 (tcgen05 {split} split of fp32 operands, fp32 accumulate: "
+        dtype_label = (f"c64 (tcgen05 3xFP16 split of fp32 operands, fp32 accumulate{', 3M products on the n, k >= 4096 steps' if any(tc_split(p) == '3M-3xFP16' for p in gemms if p['tensor_cores']) else ''}: "
                        f"{tc_share:.0%} of the step; the rest FP32 FFMA / data movement)")
     else:
         dtype_label = (f"c64 (fp32 FFMA SIMT / narrow GEMMs; tensor cores {tc_share:.0%} of the step)")

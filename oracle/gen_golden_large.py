@@ -12,6 +12,11 @@ the reference's per-slice contributions on ALL amplitudes at full size:
   config5   7x7 (1+40+1), x1 draw 0, slice 5 (64 amplitudes; peak ~35 GB)
   config4s  7x10 (1+32+1) stand-in: 1 bitstring x 1 slice (peak ~103 GB,
             only on a host with that much RAM)
+  bc60/bc70 Bristlecone-60/70 (masked 11x12, committed circuit text): one
+            bitstring (idle cells 0) x slices 0 and 1
+
+config2 / bc70 need ~52 GB: they were generated on the GPU box's host
+(GOLDEN_OUT=gpurun_out/golden, scripts/gpu_r2_golden.sh) and copied here.
 
 The GEMM is the shim's OpenBLAS cgemm (oracle/shim/Eigen/Core); the BLAS
 thread count only splits m / n blocks, so each output element's k-sum is
@@ -49,7 +54,10 @@ JOBS = {
     # under tests/golden/; parsed by the reference's own parse_circuit).
     "bc60": {"circuit": (11, 12, 32, 0), "mask": 60, "plan": "configs/config3_bristlecone60_plan.json",
              "bitstrings": 1, "slices": [0, 1]},
+    "bc70": {"circuit": (11, 12, 32, 0), "mask": 70, "plan": "configs/config4_bristlecone70_plan.json",
+             "bitstrings": 1, "slices": [0, 1]},
 }
+OUT = os.environ.get("GOLDEN_OUT", GOLD)  # e.g. gpurun_out/golden on a host with more RAM
 
 
 def cpu_model() -> str:
@@ -103,8 +111,9 @@ def run(name: str, threads: int) -> None:
             per.append(amps)
         out[f"per_slice{i}"] = np.stack(per)
         out[f"bits{i}"] = np.frombuffer("".join(bits).encode(), dtype=np.uint8).reshape(len(bits), n)
-    np.savez_compressed(os.path.join(GOLD, f"large_{name}.npz"), **out)
-    with open(os.path.join(GOLD, f"large_{name}.json"), "w") as f:
+    os.makedirs(OUT, exist_ok=True)
+    np.savez_compressed(os.path.join(OUT, f"large_{name}.npz"), **out)
+    with open(os.path.join(OUT, f"large_{name}.json"), "w") as f:
         json.dump(meta, f, indent=1)
 
 
