@@ -862,11 +862,17 @@ struct Tc5Cfg {
   // offsets (32-bit, in units of 8 complex: rows never land on output bits 0..2).
   static constexpr int EPI_WARP_FLOATS = 32 * 32;
   static constexpr int EPI_BYTES = (kWorkers / 32) * (EPI_WARP_FLOATS * 4 + 32 * 4);
-  static constexpr int SMEM_CAP = 232448 - 1024 - 256;  // 227 KiB opt-in minus alignment slack and barriers
+  static constexpr int BAR_BYTES = 512;  // mbarriers + TMEM slot
+  static constexpr int SMEM_CAP = 232448 - 1024 - BAR_BYTES;  // 227 KiB opt-in minus alignment slack and barriers
   static constexpr int STAGES =
       ((SMEM_CAP - EPI_BYTES) / STAGE_BYTES) > 6 ? 6 : ((SMEM_CAP - EPI_BYTES) / STAGE_BYTES);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + BAR_BYTES;
+  // TMEM accumulator buffers: two for 256-column tiles; narrow tiles (the
+  // HBM-bound n <= 64 steps, one k-block per tile) keep up to 8 tiles in
+  // flight so the MMA runs ahead of the per-tile epilogue / relay latency.
+  static constexpr int NBUF = BN >= 256 ? 2 : (512 / BN > 8 ? 8 : 512 / BN);
+  static constexpr int TMEM_COLS = NBUF * BN < 32 ? 32 : NBUF * BN;
+  static_assert(3 * STAGES * 8 + 2 * NBUF * 8 + 8 <= BAR_BYTES, "barrier area");
   static_assert(STAGES >= 2, "shared memory budget");
 };
 
@@ -895,9 +901,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* conv = full + Cfg::STAGES;
   uint64_t* empty = conv + Cfg::STAGES;
   uint64_t* acc_full = empty + Cfg::STAGES;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + 256);
+  uint64_t* acc_empty = acc_full + Cfg::NBUF;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(acc_empty + Cfg::NBUF);
+  float* epi_stage = reinterpret_cast<float*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::BAR_BYTES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -916,7 +922,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&conv[s], cnt);
       mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < Cfg::NBUF; ++b) {
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], cnt);
     }
@@ -1019,8 +1025,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int s = 0, c = 0;
       uint32_t ph = 0;
       for (long long q = 0; q < total_chunks; ++q) {
-        const int buf = static_cast<int>(q & 1);
-        mbar_wait_cluster(&acc_empty[buf], static_cast<uint32_t>(((q >> 1) & 1) ^ 1));
+        const int buf = static_cast<int>(q % Cfg::NBUF);
+        mbar_wait_cluster(&acc_empty[buf], static_cast<uint32_t>(((q / Cfg::NBUF) & 1) ^ 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
         const int kb_end = min(kblocks, (c + 1) * p.chunk);
@@ -1078,8 +1084,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (q >= 1) {
           const long long qq = q - 1;
-          const int buf = static_cast<int>(qq & 1);
-          mbar_wait(&acc_empty[buf], static_cast<uint32_t>((qq >> 1) & 1));
+          const int buf = static_cast<int>(qq % Cfg::NBUF);
+          mbar_wait(&acc_empty[buf], static_cast<uint32_t>((qq / Cfg::NBUF) & 1));
           mbar_arrive_remote(&acc_empty[buf], 0);
         }
       }
@@ -1194,11 +1200,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (q == 0 || p.convert_ahead) service(q, true);
       if (q >= 1) {
         const long long qq = q - 1;
-        const int buf = static_cast<int>(qq & 1);
+        const int buf = static_cast<int>(qq % Cfg::NBUF);
         if constexpr (kSplitA) {
-          mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1));
+          mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq / Cfg::NBUF) & 1));
         } else {
-          while (!__shfl_sync(0xffffffffu, mbar_test(&acc_full[buf], static_cast<uint32_t>((qq >> 1) & 1)) ? 1 : 0, 0))
+          while (!__shfl_sync(0xffffffffu, mbar_test(&acc_full[buf], static_cast<uint32_t>((qq / Cfg::NBUF) & 1)) ? 1 : 0, 0))
             service(q, false);
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
