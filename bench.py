@@ -111,14 +111,19 @@ def tc_ceiling(split, bf16):
     return {"3xFP16": bf16 / 3.0, "3M-3xFP16": bf16 * 4.0 / 9.0, "3xTF32": bf16 / 6.0}[split]
 
 
-def measured_traffic(kernel_name):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/r1_traffic.json), when it is the same launch."""
-    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        return json.load(f)["kernels"].get(kernel_name)
+def measured_traffic(kernel_name, class_key=None):
+    """DRAM bytes of the dominant kernel from a committed ncu --set full
+    capture: profiles/r2_traffic.json by class key ("<split> n=<n> k=<k>"),
+    else profiles/r1_traffic.json by the exact step name."""
+    for fname, key in (("r2_traffic.json", class_key), ("r1_traffic.json", kernel_name)):
+        p = os.path.join(ROOT, "profiles", fname)
+        if key is None or not os.path.exists(p):
+            continue
+        with open(p) as f:
+            hit = json.load(f)["kernels"].get(key)
+        if hit is not None:
+            return hit
+    return None
 
 
 def load_peaks():
@@ -636,7 +641,7 @@ def run_ours(args):
             "fp32_simt_peak_tflops": fp32_peak,
             "permute_gbs": (perm_bytes / (perm_ms / 1e3) / 1e9) if perm_ms > 0 else None,
             "permute_share_of_step": perm_ms / total_ms, "hbm_peak_gbs": peaks["hbm_gbs"]}
-    traffic = measured_traffic(kernel_name)
+    traffic = measured_traffic(kernel_name, f"{split} n={top['n']} k={top['k']}" if top["tensor_cores"] else None)
     if traffic is not None:
         roof["traffic"] = traffic["dram_read_bytes"] + traffic["dram_write_bytes"]
         roof["traffic_unit"] = "bytes per launch"
