@@ -45,10 +45,12 @@ struct BitPermParams {
 
 __device__ __forceinline__ int swz(int f) { return f ^ ((f >> 5) & 31); }
 
-__global__ void __launch_bounds__(kThreads) permute_bits_kernel(const float2* __restrict__ in,
-                                                                float2* __restrict__ out,
+// E = float2 (one complex64) or float4 (two adjacent complex64 that stay
+// adjacent: output bit 0 reads input bit 0 -- 16-byte loads and stores).
+template <typename E>
+__global__ void __launch_bounds__(kThreads) permute_bits_kernel(const E* __restrict__ in, E* __restrict__ out,
                                                                 const BitPermParams p) {
-  __shared__ float2 tile[1 << kTileBits];
+  __shared__ E tile[1 << kTileBits];
   __shared__ long long s_in_lo[32], s_in_hi[32], s_out_lo[32], s_out_hi[32];
   __shared__ unsigned short s_f_lo[32], s_f_hi[32];
   __shared__ unsigned char s_rin[kMaxBits], s_rout[kMaxBits];
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(kThreads) permute_bits_kernel(const float2* __
     base_out = static_cast<long long>((static_cast<unsigned long long>(bout_hi) << 32) | bout_lo);
   };
   constexpr int kPer = (1 << kTileBits) / kThreads;
-  float2 v[kPer];
+  E v[kPer];
   auto load = [&](long long base_in) {
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
@@ -164,6 +166,79 @@ int sm_count() {
   return n;
 }
 
+template <typename E>
+void launch_bits(const std::vector<int>& inpos, long long base, const E* src, E* dst, cudaStream_t stream,
+                 int* launches) {
+  const int r = static_cast<int>(inpos.size());
+  if (r > kMaxBits) throw std::length_error("permute: tensor rank exceeds 48 address bits");
+  std::vector<char> in_tile(static_cast<std::size_t>(r), 0);
+  std::vector<int> tile;
+  auto add = [&](int j) {
+    if (!in_tile[static_cast<std::size_t>(j)]) {
+      in_tile[static_cast<std::size_t>(j)] = 1;
+      tile.push_back(j);
+    }
+  };
+  std::vector<int> by_in(static_cast<std::size_t>(r));
+  for (int j = 0; j < r; ++j) by_in[static_cast<std::size_t>(j)] = j;
+  std::stable_sort(by_in.begin(), by_in.end(), [&](int x, int y) { return inpos[x] < inpos[y]; });
+  const int target = std::min(kTileBits, r);
+  for (int j = 0; j < std::min(5, r); ++j) add(j);
+  for (int j = 0; j < std::min(5, r) && static_cast<int>(tile.size()) < target; ++j) add(by_in[static_cast<std::size_t>(j)]);
+  for (int step = 5; static_cast<int>(tile.size()) < target; ++step) {
+    if (step < r) add(step);
+    if (static_cast<int>(tile.size()) < target && step < r) add(by_in[static_cast<std::size_t>(step)]);
+  }
+  const int t = static_cast<int>(tile.size());
+  std::vector<int> load_order = tile, store_order = tile;
+  std::sort(load_order.begin(), load_order.end(), [&](int x, int y) { return inpos[x] < inpos[y]; });
+  std::sort(store_order.begin(), store_order.end());
+  std::vector<int> store_rank(static_cast<std::size_t>(r), -1);
+  for (int k = 0; k < t; ++k) store_rank[static_cast<std::size_t>(store_order[static_cast<std::size_t>(k)])] = k;
+
+  BitPermParams p;
+  std::memset(&p, 0, sizeof p);
+  p.in_base = base;
+  p.tbits = t;
+  for (int e = 0; e < 32; ++e) {
+    long long ilo = 0, ihi = 0, olo = 0, ohi = 0;
+    unsigned flo = 0, fhi = 0;
+    for (int k = 0; k < 5; ++k) {
+      if (!((e >> k) & 1)) continue;
+      if (k < t) {
+        const int j = load_order[static_cast<std::size_t>(k)];
+        ilo += 1ll << inpos[static_cast<std::size_t>(j)];
+        flo |= 1u << store_rank[static_cast<std::size_t>(j)];
+        olo += 1ll << store_order[static_cast<std::size_t>(k)];
+      }
+      if (k + 5 < t) {
+        const int j = load_order[static_cast<std::size_t>(k + 5)];
+        ihi += 1ll << inpos[static_cast<std::size_t>(j)];
+        fhi |= 1u << store_rank[static_cast<std::size_t>(j)];
+        ohi += 1ll << store_order[static_cast<std::size_t>(k + 5)];
+      }
+    }
+    p.in_lo[e] = ilo;
+    p.in_hi[e] = ihi;
+    p.out_lo[e] = olo;
+    p.out_hi[e] = ohi;
+    p.f_lo[e] = static_cast<unsigned short>(flo);
+    p.f_hi[e] = static_cast<unsigned short>(fhi);
+  }
+  int nrest = 0;
+  for (int j = 0; j < r; ++j)
+    if (!in_tile[static_cast<std::size_t>(j)]) {
+      p.rest_in[nrest] = static_cast<unsigned char>(inpos[static_cast<std::size_t>(j)]);
+      p.rest_out[nrest] = static_cast<unsigned char>(j);
+      ++nrest;
+    }
+  p.nrest = nrest;
+  p.ntiles = 1ll << nrest;
+  const long long grid = std::min<long long>(p.ntiles, static_cast<long long>(sm_count()) * 8);
+  permute_bits_kernel<E><<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(src, dst, p);
+  if (launches) ++*launches;
+}
+
 }  // namespace
 
 cudaError_t permute(const void* in, std::int64_t base, void* out, int rank, const std::int64_t* extent,
@@ -187,74 +262,17 @@ cudaError_t permute(const void* in, std::int64_t base, void* out, int rank, cons
       const int s = extent[a] > 1 ? ilog2(istride[a]) : 0;
       for (int b = 0; b < w; ++b) inpos.push_back(s + b);
     }
-    const int r = static_cast<int>(inpos.size());
-    if (r > kMaxBits) throw std::length_error("permute: tensor rank exceeds 48 address bits");
-    std::vector<char> in_tile(static_cast<std::size_t>(r), 0);
-    std::vector<int> tile;
-    auto add = [&](int j) {
-      if (!in_tile[static_cast<std::size_t>(j)]) {
-        in_tile[static_cast<std::size_t>(j)] = 1;
-        tile.push_back(j);
-      }
-    };
-    std::vector<int> by_in(static_cast<std::size_t>(r));
-    for (int j = 0; j < r; ++j) by_in[static_cast<std::size_t>(j)] = j;
-    std::stable_sort(by_in.begin(), by_in.end(), [&](int x, int y) { return inpos[x] < inpos[y]; });
-    const int target = std::min(kTileBits, r);
-    for (int j = 0; j < std::min(5, r); ++j) add(j);
-    for (int j = 0; j < std::min(5, r) && static_cast<int>(tile.size()) < target; ++j) add(by_in[static_cast<std::size_t>(j)]);
-    for (int step = 5; static_cast<int>(tile.size()) < target; ++step) {
-      if (step < r) add(step);
-      if (static_cast<int>(tile.size()) < target && step < r) add(by_in[static_cast<std::size_t>(step)]);
+    if (static_cast<int>(inpos.size()) > kMaxBits) throw std::length_error("permute: tensor rank exceeds 48 address bits");
+    // Element pairs that stay adjacent move as 16-byte units.
+    const bool pairs = inpos.size() >= 2 && inpos[0] == 0 && base % 2 == 0 &&
+                       reinterpret_cast<std::uintptr_t>(in) % 16 == 0 && reinterpret_cast<std::uintptr_t>(out) % 16 == 0;
+    if (pairs) {
+      std::vector<int> half(inpos.begin() + 1, inpos.end());
+      for (auto& x : half) --x;
+      launch_bits<float4>(half, base / 2, static_cast<const float4*>(in), static_cast<float4*>(out), stream, launches);
+    } else {
+      launch_bits<float2>(inpos, base, src, dst, stream, launches);
     }
-    const int t = static_cast<int>(tile.size());
-    std::vector<int> load_order = tile, store_order = tile;
-    std::sort(load_order.begin(), load_order.end(), [&](int x, int y) { return inpos[x] < inpos[y]; });
-    std::sort(store_order.begin(), store_order.end());
-    std::vector<int> store_rank(static_cast<std::size_t>(r), -1);
-    for (int k = 0; k < t; ++k) store_rank[static_cast<std::size_t>(store_order[static_cast<std::size_t>(k)])] = k;
-
-    BitPermParams p;
-    std::memset(&p, 0, sizeof p);
-    p.in_base = base;
-    p.tbits = t;
-    for (int e = 0; e < 32; ++e) {
-      long long ilo = 0, ihi = 0, olo = 0, ohi = 0;
-      unsigned flo = 0, fhi = 0;
-      for (int k = 0; k < 5; ++k) {
-        if (!((e >> k) & 1)) continue;
-        if (k < t) {
-          const int j = load_order[static_cast<std::size_t>(k)];
-          ilo += 1ll << inpos[static_cast<std::size_t>(j)];
-          flo |= 1u << store_rank[static_cast<std::size_t>(j)];
-          olo += 1ll << store_order[static_cast<std::size_t>(k)];
-        }
-        if (k + 5 < t) {
-          const int j = load_order[static_cast<std::size_t>(k + 5)];
-          ihi += 1ll << inpos[static_cast<std::size_t>(j)];
-          fhi |= 1u << store_rank[static_cast<std::size_t>(j)];
-          ohi += 1ll << store_order[static_cast<std::size_t>(k + 5)];
-        }
-      }
-      p.in_lo[e] = ilo;
-      p.in_hi[e] = ihi;
-      p.out_lo[e] = olo;
-      p.out_hi[e] = ohi;
-      p.f_lo[e] = static_cast<unsigned short>(flo);
-      p.f_hi[e] = static_cast<unsigned short>(fhi);
-    }
-    int nrest = 0;
-    for (int j = 0; j < r; ++j)
-      if (!in_tile[static_cast<std::size_t>(j)]) {
-        p.rest_in[nrest] = static_cast<unsigned char>(inpos[static_cast<std::size_t>(j)]);
-        p.rest_out[nrest] = static_cast<unsigned char>(j);
-        ++nrest;
-      }
-    p.nrest = nrest;
-    p.ntiles = 1ll << nrest;
-    const long long grid = std::min<long long>(p.ntiles, static_cast<long long>(sm_count()) * 8);
-    permute_bits_kernel<<<static_cast<unsigned>(grid), kThreads, 0, stream>>>(src, dst, p);
-    if (launches) ++*launches;
     return cudaGetLastError();
   }
 
