@@ -55,11 +55,14 @@ def stats(got, truth):
     got, truth = np.asarray(got).reshape(-1), np.asarray(truth).reshape(-1)
     nz = truth != 0  # structurally vanishing contributions (inconsistent cut digits) must come out ~0
     rel = np.abs(np.abs(got[nz]) - np.abs(truth[nz])) / np.abs(truth[nz])
-    fid = abs(np.vdot(got, truth)) ** 2 / (np.vdot(got, got).real * np.vdot(truth, truth).real)
-    return {"rel_l2": float(np.linalg.norm(got - truth) / np.linalg.norm(truth)),
-            "max_rel_abs": float(rel.max()), "fidelity_deficit": float(1 - fid),
+    ng, nt = np.vdot(got, got).real, np.vdot(truth, truth).real
+    fid = abs(np.vdot(got, truth)) ** 2 / (ng * nt) if ng > 0 and nt > 0 else float(ng == nt)
+    scale = np.linalg.norm(truth) if nt > 0 else 1.0
+    return {"rel_l2": float(np.linalg.norm(got - truth) / scale),
+            "max_rel_abs": float(rel.max()) if nz.any() else 0.0, "fidelity_deficit": float(1 - fid),
             "zero_entries": int((~nz).sum()), "max_abs_at_zeros": float(np.abs(got[~nz]).max()) if (~nz).any() else 0.0,
-            "min_abs_over_rms": float(np.abs(truth[nz]).min() / np.sqrt(np.mean(np.abs(truth) ** 2)))}
+            "min_abs_over_rms": float(np.abs(truth[nz]).min() / np.sqrt(np.mean(np.abs(truth) ** 2)))
+            if nz.any() else 0.0}
 
 
 def engine_per_slice(gpu, text, plan_text, x1, slices, tc):
