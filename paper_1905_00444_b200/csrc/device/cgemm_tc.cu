@@ -72,6 +72,7 @@ constexpr int kThreads = 64 + kWorkers;   // + producer warp + MMA warp
 // grows linearly with the reduction length (measured ~1.4e-8 * k); 32
 // complex K per chunk keeps it at the 3xTF32 floor (~5e-7).
 constexpr int kChunkDefault = 4;  // QSG_TC_CHUNK overrides (experiments)
+constexpr int kShortKChunks = 1;  // promotion chunks of a k <= 256 tile (QSG_TC_SHORTK_CHUNKS)
 constexpr int A_BYTES = BM * BK * 4;
 
 template <int BN>
@@ -1740,7 +1741,14 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   const char* chunk_env = std::getenv("QSG_TC_CHUNK");
   const int per128 = 128 / kb;  // k-blocks per 128 real K
   if (chunk_env) p.chunk = std::max(1, chunk_blocks() * per128 / 4);
-  else p.chunk = p.kblocks <= 4 * per128 ? p.kblocks : per128;
+  else if (p.kblocks <= 4 * per128) {
+    // Short K (<= 512 real K): QSG_TC_SHORTK_CHUNKS promotion chunks per tile
+    // (1 = one unpromoted TMEM chunk, stored straight from TMEM).
+    const int parts = std::min(env_int("QSG_TC_SHORTK_CHUNKS", kShortKChunks), p.kblocks);
+    p.chunk = (p.kblocks + parts - 1) / parts;
+  } else {
+    p.chunk = per128;
+  }
   p.store_perm = g.store_perm ? 1 : 0;
   p.nrow_bits = g.nrow_bits;
   p.ncol_bits = g.ncol_bits;

@@ -15,3 +15,5 @@ CMD="python bench.py --steps 1 --warmup 0 --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final/ncu_launches_c5.csv $CMD > gpurun_out/final/ncu_list.log 2>&1; echo "ncu list rc=$?"
 IDX=$(python scripts/ncu_pick.py gpurun_out/final/ncu_launches_c5.csv cgemm_f16_pair_kernel --summary 2> gpurun_out/final/ncu_launches_c5_summary.txt); echo "idx=$IDX"; head -8 gpurun_out/final/ncu_launches_c5_summary.txt
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cgemm_f16_pair_kernel -s $IDX -c 1 -o gpurun_out/final/ncu_full_c5_cube $CMD > gpurun_out/final/ncu_full.log 2>&1; echo "ncu rc=$?"
+# config 1: per-launch durations of one widened contraction (latency floor evidence)
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/final/ncu_launches_c1.csv python bench.py --config 1 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/final/ncu_c1.log 2>&1; echo "ncu c1 rc=$?"

@@ -80,7 +80,7 @@ CASES = {
     "config3s": ((6, 10, 32, 0), "configs/config3_standin_6x10_plan.json", [0, 1], "large_config3s"),
     # Bristlecone-60 (masked 11x12 embedding, circuit text committed)
     "bc60": (("mask", 60), "configs/config3_bristlecone60_plan.json", [0, 1], "large_bc60"),
-    "bc70": (("mask", 70), "configs/config4_bristlecone70_plan.json", [0, 1], "large_bc70"),
+    "bc70": (("mask", 70), "configs/config4_bristlecone70_plan.json", [2, 6], "large_bc70"),
 }
 
 
