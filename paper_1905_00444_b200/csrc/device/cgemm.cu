@@ -325,10 +325,22 @@ int sm_count() {
 int choose_splits(std::int64_t m, std::int64_t n, std::int64_t k) {
   const std::int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   const std::int64_t want = 2 * static_cast<std::int64_t>(sm_count());
-  if (tiles >= want || k < 512) return 1;
-  std::int64_t s = std::min<std::int64_t>((want + tiles - 1) / tiles, k / 256);
-  // Cap the partial buffer at 1 GiB.
-  while (s > 1 && s * m * n * 8 > (std::int64_t{1} << 30)) --s;
+  std::int64_t s = 1;
+  if (tiles < want && k >= 512) {
+    s = std::min<std::int64_t>((want + tiles - 1) / tiles, k / 256);
+    // Cap the occupancy partial buffer at 1 GiB.
+    while (s > 1 && s * m * n * 8 > (std::int64_t{1} << 30)) --s;
+  }
+  // Accuracy: one FFMA chain per output element over the whole of a long K
+  // grows its rounding error with K (config 2's k = 32768 / 65536 steps put
+  // the FP32 engine's smallest amplitude at 1.5e-4 relative); K/4096-way
+  // split-K with the ordered fp32 reduction bounds every chain at 4096
+  // terms.  Partial buffers up to 16 GiB (s026: 8 x 2 GiB).
+  if (k >= 8192) {
+    std::int64_t sa = std::min<std::int64_t>(16, k / 4096);
+    while (sa > 1 && sa * m * n * 8 > (std::int64_t{16} << 30)) --sa;
+    s = std::max(s, sa);
+  }
   return static_cast<int>(std::max<std::int64_t>(s, 1));
 }
 

@@ -72,7 +72,7 @@ constexpr int kThreads = 64 + kWorkers;   // + producer warp + MMA warp
 // grows linearly with the reduction length (measured ~1.4e-8 * k); 32
 // complex K per chunk keeps it at the 3xTF32 floor (~5e-7).
 constexpr int kChunkDefault = 4;  // QSG_TC_CHUNK overrides (experiments)
-constexpr int kShortKChunks = 1;  // promotion chunks of a k <= 256 tile (QSG_TC_SHORTK_CHUNKS)
+constexpr int kShortKChunks = 2;  // promotion chunks of a k <= 256 tile (QSG_TC_SHORTK_CHUNKS; 1 = fastest, see DESIGN 2)
 constexpr int A_BYTES = BM * BK * 4;
 
 template <int BN>
