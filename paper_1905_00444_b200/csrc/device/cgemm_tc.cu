@@ -1095,9 +1095,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else {
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    float acc[kDirect == 1 ? 1 : HALF];
+    // kDirect 1 / 3 read the accumulator straight from TMEM in the epilogue
+    // (3: the tile's two promotion chunks sit in consecutive ring buffers
+    // and are summed there, in round-to-nearest fp32, per 16-column slab).
+    constexpr bool kFromTmem = kDirect == 1 || kDirect == 3;
+    float acc[kFromTmem ? 1 : HALF];
 #pragma unroll
-    for (int i = 0; i < (kDirect == 1 ? 1 : HALF); ++i) acc[i] = 0.f;
+    for (int i = 0; i < (kFromTmem ? 1 : HALF); ++i) acc[i] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(quad * 32) << 16) + static_cast<uint32_t>(half * HALF);
     const int sa = tc_pending_shift(p.meta_a, p.norm_a), sb = tc_pending_shift(p.meta_b, p.norm_b);
     const int ea = p.a_presplit ? p.meta_a->split_exp : f16_exp(p.meta_a), eb = f16_exp(p.meta_b);
@@ -1234,7 +1238,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
-        if (kDirect || qq % nchunks == nchunks - 1) {
+        const int prev = static_cast<int>((qq + Cfg::NBUF - 1) % Cfg::NBUF);  // kDirect 3: the tile's first chunk
+        // 16 accumulator columns of this lane's row straight from TMEM.
+        auto tmem16 = [&](int col, float* v) {
+          tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + col), v);
+          if constexpr (kDirect == 3) {
+            float w[16];
+            tmem_ld16(lane_base + static_cast<uint32_t>(prev * kPairBN + col), w);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = w[i] + v[i];
+          }
+        };
+        if (kDirect == 1 || kDirect == 2 || qq % nchunks == nchunks - 1) {
           long long m_pair;
           int n_tile;
           pair_tile_coords(cluster + (qq / nchunks) * nclusters, m_pairs, p.n_tiles, m_pair, n_tile, p.group_m);
@@ -1277,8 +1292,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int h16 = 0; h16 < 2; ++h16) {
                   float a16[16];
-                  if constexpr (kDirect == 1) {
-                    tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0 + 16 * h16), a16);
+                  if constexpr (kFromTmem) {
+                    tmem16(c0 + 16 * h16, a16);
                   } else {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) a16[i] = acc[c0 + 16 * h16 + i];
@@ -1339,8 +1354,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int c0 = 0; c0 < HALF; c0 += 16) {
             if ((c0 & 31) == 0) service(q, false);
             float a16[16];
-            if constexpr (kDirect == 1) {
-              tmem_ld16(lane_base + static_cast<uint32_t>(buf * kPairBN + c0), a16);
+            if constexpr (kFromTmem) {
+              tmem16(c0, a16);
             } else {
 #pragma unroll
               for (int i = 0; i < 16; ++i) a16[i] = acc[c0 + i];
@@ -1408,9 +1423,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             __syncwarp();
           }
           }
-          if constexpr (kDirect == 1) {
+          if constexpr (kFromTmem) {
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+            if (lane == 0) {
+              mbar_arrive(&acc_empty[buf]);
+              if constexpr (kDirect == 3) mbar_arrive(&acc_empty[prev]);
+            }
           } else if constexpr (kDirect == 0) {
 #pragma unroll
             for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
@@ -1618,6 +1636,23 @@ int pair_bn(std::int64_t n) {
   return 0;
 }
 
+// Short-K tiles promoted in two chunks run as 128-column tiles whose two
+// chunk accumulators are summed in the epilogue straight from TMEM
+// (kDirect 3: 4 ring buffers of 128 columns) instead of through 128
+// promotion registers per thread (QSG_TC_DIRECT2=0: the register path).
+bool two_chunk_direct(std::int64_t k) {
+  const char* env = std::getenv("QSG_TC_DIRECT2");
+  if (env && env[0] == '0') return false;
+  const std::int64_t kblocks = (2 * k + BK16 - 1) / BK16;
+  return kblocks <= 8 && kblocks >= 2 && std::min<std::int64_t>(env_int("QSG_TC_SHORTK_CHUNKS", kShortKChunks), kblocks) == 2;
+}
+
+// Column tile of the fp16 pair kernel for a GEMM shape.
+int f16_bn(std::int64_t n, std::int64_t k) {
+  const int bn = pair_bn(n);
+  return (bn == 256 && two_chunk_direct(k)) ? 128 : bn;
+}
+
 bool use_pair(std::int64_t m, std::int64_t n) {
   const char* env = std::getenv("QSG_TC_2SM");
   if (env && env[0] == '0') return false;
@@ -1676,7 +1711,7 @@ std::int64_t sync_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   const int every = sync_every();
   const std::int64_t kblocks = (2 * k + BK16 - 1) / BK16;
   if (every <= 0 || !use_pair(m, n)) return 0;
-  const std::int64_t tiles = (m / 256) * ((2 * n) / pair_bn(n));
+  const std::int64_t tiles = (m / 256) * ((2 * n) / f16_bn(n, k));
   return ((((tiles * kblocks) / every + 2) * 4 + 255) / 256) * 256;  // checkpoints of the longest run (1 pair)
 }
 
@@ -1763,6 +1798,16 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                          Tc5Cfg<BN>::SMEM);
     return resident_pairs(cgemm_f16_pair_kernel<BN, false>, Tc5Cfg<BN>::SMEM);
   }();
+  static const bool attrs_direct3 = [] {
+    if constexpr (BN <= 128) {
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Tc5Cfg<BN>::SMEM);
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Tc5Cfg<BN>::SMEM);
+    }
+    return true;
+  }();
+  (void)attrs_direct3;
   static const bool attrs_direct = [] {
     cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Tc5Cfg<BN>::SMEM);
@@ -1780,6 +1825,17 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   const bool direct = p.kblocks <= p.chunk && !(std::getenv("QSG_TC_DIRECT") && std::getenv("QSG_TC_DIRECT")[0] == '0');
   // Early TMEM release for single-chunk tiles (QSG_TC_EARLY=0: slab-by-slab reads).
   static const bool early = std::getenv("QSG_TC_EARLY") && std::getenv("QSG_TC_EARLY")[0] == '1';
+  const bool direct3 = !direct && BN <= 128 && p.kblocks <= 8 && (p.kblocks + p.chunk - 1) / p.chunk == 2 &&
+                       two_chunk_direct(g.k);
+  if constexpr (BN <= 128) {
+    if (direct3) {
+      if (split)
+        cgemm_f16_pair_kernel<BN, true, BK16, 3><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+      else
+        cgemm_f16_pair_kernel<BN, false, BK16, 3><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+      return cudaGetLastError();
+    }
+  }
   if (direct && split && early)
     cgemm_f16_pair_kernel<BN, true, BK16, 2><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
   else if (direct && early)
@@ -1993,7 +2049,7 @@ cudaError_t cgemm_tc_3m(const GemmArgs& g, const TMeta* ma, const TMeta* mb, cud
     }
     const __half* ahi = static_cast<const __half*>(r.a);
     const __half* alo = ahi + mk;
-    switch (pair_bn(r.n)) {
+    switch (f16_bn(r.n, r.k)) {
       case 256: e = launch_f16_pair<256>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
       case 128: e = launch_f16_pair<128>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
       case 64: e = launch_f16_pair<64>(r, meta_a3, meta_b3, bhi, blo, sync, ahi, alo, stream); break;
@@ -2130,7 +2186,7 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
       if (launches) ++*launches;
     }
     cudaError_t e = cudaSuccess;
-    switch (pair_bn(g.n)) {
+    switch (f16_bn(g.n, g.k)) {
       case 256: e = launch_f16_pair<256>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
       case 128: e = launch_f16_pair<128>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
       case 64: e = launch_f16_pair<64>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
