@@ -39,9 +39,14 @@ def fp64_slice(text, plan, x1, slice_id):
     for i, (lhs, rhs) in enumerate(plan["order"]):
         (la, a), (lb, b) = live.pop(lhs), live.pop(rhs)
         shared = [x for x in la if x in lb]
-        c = torch.tensordot(a, b, dims=([la.index(x) for x in shared], [lb.index(x) for x in shared]))
+        lc = [x for x in la if x not in shared] + [x for x in lb if x not in shared]
+        if a.dim() == 0 or b.dim() == 0:  # scalar factor (idle Bristlecone cells): torch.tensordot adds a dim
+            c = a * b
+        else:
+            c = torch.tensordot(a, b, dims=([la.index(x) for x in shared], [lb.index(x) for x in shared]))
+        c = c.reshape([2] * len(lc))
         del a, b
-        live[f"s{i:03d}"] = ([x for x in la if x not in shared] + [x for x in lb if x not in shared], c)
+        live[f"s{i:03d}"] = (lc, c)
     (lab, t), = live.values()
     perm = sorted(range(len(lab)), key=lambda j: lab[j])
     out = t.permute(perm).reshape(-1) if lab else t.reshape(-1)
