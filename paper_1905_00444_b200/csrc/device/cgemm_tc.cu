@@ -1636,13 +1636,15 @@ int pair_bn(std::int64_t n) {
   return 0;
 }
 
-// Short-K tiles promoted in two chunks run as 128-column tiles whose two
-// chunk accumulators are summed in the epilogue straight from TMEM
-// (kDirect 3: 4 ring buffers of 128 columns) instead of through 128
-// promotion registers per thread (QSG_TC_DIRECT2=0: the register path).
+// QSG_TC_DIRECT2=1: short-K tiles promoted in two chunks run as 128-column
+// tiles whose two chunk accumulators are summed in the epilogue straight
+// from TMEM (kDirect 3: 4 ring buffers of 128 columns) instead of through
+// 128 promotion registers per thread.  Measured 3-4% slower than the
+// register path on configs 2/3/4 (the 128-column tiles cost more than the
+// registers), so off by default.
 bool two_chunk_direct(std::int64_t k) {
   const char* env = std::getenv("QSG_TC_DIRECT2");
-  if (env && env[0] == '0') return false;
+  if (!(env && env[0] == '1')) return false;
   const std::int64_t kblocks = (2 * k + BK16 - 1) / BK16;
   return kblocks <= 8 && kblocks >= 2 && std::min<std::int64_t>(env_int("QSG_TC_SHORTK_CHUNKS", kShortKChunks), kblocks) == 2;
 }
