@@ -44,6 +44,11 @@ typedef enum qsg_status {
 
 const char* qsg_last_error(void);
 int qsg_last_error_line(void);
+/* Slice of a failed job (qsg_run_amplitudes): the lowest failing task's
+ * slice id, also appended to the message as " (slice N)" -- the reference's
+ * JobError (include/qsim/engine.hpp:81-84, src/engine.cpp:38-39, 247-283).
+ * -1 when the last error was not attributed to a slice. */
+int64_t qsg_last_error_slice(void);
 const char* qsg_version(void);
 int qsg_device_count(int* count);
 

@@ -54,6 +54,15 @@ class LengthError(QsgError, ValueError):
     pass
 
 
+class JobError(QsgError):
+    """A run_amplitudes job failed; slice_id = the lowest failing task's
+    slice (the reference's JobError, include/qsim/engine.hpp:81-84)."""
+
+    def __init__(self, code, msg, slice_id):
+        super().__init__(code, msg)
+        self.slice_id = slice_id
+
+
 class OutOfRange(QsgError, IndexError):
     pass
 
@@ -102,6 +111,7 @@ def lib():
     sig = {
         "qsg_last_error": (cp, []),
         "qsg_last_error_line": (i32, []),
+        "qsg_last_error_slice": (i64, []),
         "qsg_version": (cp, []),
         "qsg_device_count": (i32, [P(i32)]),
         "qsg_mix_seed": (u64, [u64, u64]),
@@ -186,6 +196,9 @@ def _check(rc: int):
         raise LengthError(rc, msg)
     if rc == 3:
         raise OutOfRange(rc, msg)
+    slice_id = L.qsg_last_error_slice()
+    if slice_id >= 0:
+        raise JobError(rc, msg, slice_id)
     raise QsgError(rc, msg)
 
 

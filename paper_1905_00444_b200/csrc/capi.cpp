@@ -28,12 +28,18 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int g_err_line = 0;
+thread_local std::int64_t g_err_slice = -1;
 
 template <class F>
 int guarded(F&& f) {
+  g_err_slice = -1;
   try {
     f();
     return QSG_OK;
+  } catch (const qsg::JobError& e) {
+    g_err = e.what();
+    g_err_slice = e.slice_id;
+    return QSG_ERR_RUNTIME;
   } catch (const qsg::CircuitError& e) {
     g_err = e.what();
     g_err_line = e.line;
@@ -153,6 +159,7 @@ extern "C" {
 
 const char* qsg_last_error(void) { return g_err.c_str(); }
 int qsg_last_error_line(void) { return g_err_line; }
+int64_t qsg_last_error_slice(void) { return g_err_slice; }
 const char* qsg_version(void) { return "qsg 0.1 (sm_100a)"; }
 
 int qsg_device_count(int* count) {

@@ -974,7 +974,25 @@ void Engine::run(const std::vector<std::int64_t>& slice_ids, bool reset, bool pe
 
 void Engine::enqueue_run(const std::vector<std::int64_t>& slice_ids, bool reset, bool per_slice) {
   if (reset) check(cudaMemsetAsync(acc_, 0, sizeof(double2) * static_cast<std::size_t>(batch_), stream_), "acc reset");
+  // QSG_FAIL_SLICES=a,b,...: fault injection for the failure-attribution
+  // tests (a run that reaches one of these slices throws).
+  static const std::vector<std::int64_t> fail = [] {
+    std::vector<std::int64_t> v;
+    if (const char* env = std::getenv("QSG_FAIL_SLICES")) {
+      std::string t(env);
+      std::size_t pos = 0;
+      while (pos < t.size()) {
+        const std::size_t c = t.find(',', pos);
+        v.push_back(std::stoll(t.substr(pos, c == std::string::npos ? std::string::npos : c - pos)));
+        if (c == std::string::npos) break;
+        pos = c + 1;
+      }
+    }
+    return v;
+  }();
   for (std::size_t s = 0; s < slice_ids.size(); ++s) {
+    if (!fail.empty() && std::find(fail.begin(), fail.end(), slice_ids[s]) != fail.end())
+      throw std::runtime_error("injected failure");
     const auto digits = cut_digits(shape_, plan_.cut, slice_ids[s]);
     std::vector<std::int64_t> node_off(node_x1_off_);
     for (std::size_t q = 0; q < node_vol_.size(); ++q)
@@ -1282,9 +1300,25 @@ AmplitudeOutput run_amplitudes(Engine& e, const std::vector<std::string>& bitstr
       bits[static_cast<std::size_t>(q)] = b[static_cast<std::size_t>(q)] - '0';
     }
     e.prepare(bits);
-    e.run(out.slice_ids, true, false);
     std::vector<cdouble> amps;
-    e.results(&amps, nullptr);
+    try {
+      e.run(out.slice_ids, true, false);
+      e.results(&amps, nullptr);
+    } catch (const std::exception& ex) {
+      // The batch runs asynchronously; attribute the failure the way the
+      // reference's schedule() does (lowest failing task): re-run the
+      // slices one at a time, synchronously, and report the first that fails.
+      const std::string first = ex.what();
+      for (const auto id : out.slice_ids) {
+        try {
+          e.run({id}, true, false);
+          e.synchronize();
+        } catch (const std::exception& ex2) {
+          throw JobError(ex2.what(), id);
+        }
+      }
+      throw JobError(first, out.slice_ids.empty() ? -1 : out.slice_ids.front());
+    }
     out.amplitudes.emplace_back(b, amps[0]);
     out.total_flops += e.plan().flops_per_slice * out.slice_ids.size();
   }

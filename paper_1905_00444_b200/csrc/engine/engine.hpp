@@ -250,6 +250,15 @@ class Engine {
 std::vector<std::pair<std::string, cdouble>> amplitude_batch(Engine& e, const std::vector<int>& x1_bits,
                                                              const std::vector<std::int64_t>& slice_ids);
 
+// run_amplitudes failure attributed to a slice, as the reference's JobError
+// (include/qsim/engine.hpp:81-84, src/engine.cpp:38-39): message +
+// " (slice N)", N = the slice of the lowest failing task (src/engine.cpp:247-283).
+struct JobError : std::runtime_error {
+  JobError(const std::string& msg, std::int64_t slice)
+      : std::runtime_error(msg + " (slice " + std::to_string(slice) + ")"), slice_id(slice) {}
+  std::int64_t slice_id;
+};
+
 struct AmplitudeOutput {
   std::vector<std::pair<std::string, cdouble>> amplitudes;
   std::vector<std::int64_t> slice_ids;

@@ -130,6 +130,39 @@ def test_run_amplitudes_closed_plan(gpu):
         assert ids2 == gpu.select_slices(k, pj["slices"], pj["slices"], 3)
 
 
+_JOB_CHILD = r"""
+import json, sys
+sys.path.insert(0, sys.argv[1])
+import paper_1905_00444_b200 as Q
+text = Q.generate_rqc(4, 4, 10, 5)
+plan = Q.plan_json(text, [], Q.PLAN_GREEDY, "", 2048)
+bits = ["0" * 16, "1" * 16]
+with Q.Engine(text, plan) as e:
+    try:
+        e.run_amplitudes(bits)
+        print(json.dumps({"raised": None}))
+    except Q.JobError as err:
+        print(json.dumps({"raised": "JobError", "slice": err.slice_id, "msg": str(err)}))
+"""
+
+
+def test_run_amplitudes_failure_names_lowest_failing_slice(gpu):
+    """SURVEY 5 failure detection / SPEC "worker panic -> job fails with the
+    offending slice_id": a run_amplitudes job whose slices 3 and 1 fail
+    (fault injection, QSG_FAIL_SLICES, in a fresh process) raises JobError
+    for slice 1 -- the lowest failing task, as the reference's schedule()
+    reports it (src/engine.cpp:247-283) -- with " (slice 1)" in the message."""
+    import subprocess
+    import sys
+    env = dict(os.environ, QSG_FAIL_SLICES="3,1")
+    res = subprocess.run([sys.executable, "-c", _JOB_CHILD, ROOT], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = json.loads(res.stdout.strip().splitlines()[-1])
+    assert got["raised"] == "JobError" and got["slice"] == 1, got
+    assert got["msg"].endswith("(slice 1)"), got
+
+
 def test_engine_rejects_bad_inputs(gpu, cases):
     am, meta = cases
     case = meta["cases"][0]
