@@ -1711,7 +1711,7 @@ int sync_every() {
 // tiles on one pair); 0 when K-sync is off.
 std::int64_t sync_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
   const int every = sync_every();
-  const std::int64_t kblocks = (2 * k + BK16 - 1) / BK16;
+  const std::int64_t kblocks = (2 * k + 31) / 32;  // 32-K stages (QSG_TC_STAGEK=32) count twice the 64-K blocks
   if (every <= 0 || !use_pair(m, n)) return 0;
   const std::int64_t tiles = (m / 256) * ((2 * n) / f16_bn(n, k));
   return ((((tiles * kblocks) / every + 2) * 4 + 255) / 256) * 256;  // checkpoints of the longest run (1 pair)
@@ -1737,9 +1737,12 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
                             cudaStream_t stream) {
   const bool split = ahi != nullptr;
   // 64-K stages (3 in flight).  32-K stages (6 in flight, SW64 planes; the
-  // kernel's kBK = 32 instantiation) measured 2-6% slower: the per-stage
-  // barrier / commit overhead outweighs the deeper TMA lookahead.
-  const int kb = BK16;
+  // kernel's kBK = 32 instantiation) measured 2-6% slower on the long-K
+  // steps: the per-stage barrier / commit overhead outweighs the deeper TMA
+  // lookahead.  QSG_TC_STAGEK=32 selects them for short-K (k <= 256)
+  // pre-split tiles, whose A streams from HBM (more bytes in flight).
+  static const bool stage32 = env_int("QSG_TC_STAGEK", 64) == 32;
+  const int kb = (split && stage32 && 2 * g.k <= 512) ? 32 : BK16;
   const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM, kb) : make_map(g.a, 2 * g.k, g.m, BM);
   const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM, kb) : ma;
   const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
@@ -1827,6 +1830,21 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   const bool direct = p.kblocks <= p.chunk && !(std::getenv("QSG_TC_DIRECT") && std::getenv("QSG_TC_DIRECT")[0] == '0');
   // Early TMEM release for single-chunk tiles (QSG_TC_EARLY=0: slab-by-slab reads).
   static const bool early = std::getenv("QSG_TC_EARLY") && std::getenv("QSG_TC_EARLY")[0] == '1';
+  if (kb == 32) {
+    static const bool attrs32 = [] {
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, 32, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Tc5Cfg<BN, 32>::SMEM);
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, 32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Tc5Cfg<BN, 32>::SMEM);
+      return true;
+    }();
+    (void)attrs32;
+    if (direct)
+      cgemm_f16_pair_kernel<BN, true, 32, 1><<<grid, kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    else
+      cgemm_f16_pair_kernel<BN, true, 32, 0><<<grid, kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    return cudaGetLastError();
+  }
   const bool direct3 = !direct && BN <= 128 && p.kblocks <= 8 && (p.kblocks + p.chunk - 1) / p.chunk == 2 &&
                        two_chunk_direct(g.k);
   if constexpr (BN <= 128) {
