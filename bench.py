@@ -535,7 +535,7 @@ def run_ours(args):
     eng.fold_nodes(text, out=host_nodes)
     host_x1 = [np.asarray([draw(0, 0) if slice_mode else
                            draw(1, (rank * args.steps + i) * xb + t) for t in range(xb)],
-                          dtype=np.int32) for i in range(args.steps)]
+                          dtype=np.int32) for i in range(max(args.steps, 2))]
     def e2e_step(i):
         eng.load_nodes(host_nodes)
         if xb == 1:
