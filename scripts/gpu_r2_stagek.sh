@@ -10,3 +10,5 @@ for r in 1 2; do
     done
   done
 done
+# config 1: per-launch durations + DRAM bytes of one widened contraction (latency-floor evidence)
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/stk/ncu_launches_c1.csv python bench.py --config 1 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/stk/ncu_c1.log 2>&1; echo "ncu c1 rc=$?"
