@@ -46,6 +46,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "kernels_tc.hpp"
 
@@ -104,6 +105,7 @@ struct TcParams {
   int stream_store;    // fp16 kernel: evict-first (st.global.cs) output stores
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int passes;         // fp16 kernel: 3 (hi.hi + hi.lo + lo.hi); 2 = power-model experiment only (QSG_TC_PASSES)
+  unsigned long long* prof;  // fp16 pair kernel, QSG_TC_PROF=1: per-CTA role wait / busy cycle counters
   int convert_ahead;  // fp16 kernel, raw A: convert a chunk's stages before the previous chunk's epilogue (A/B knob)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
@@ -944,6 +946,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base_slot;
+  // QSG_TC_PROF counters (lane 0 of each role): [0] producer waiting for a
+  // free stage, [1] MMA waiting for a TMEM buffer, [2] MMA waiting for a
+  // landed stage, [3] workers waiting for a full accumulator, [4] workers
+  // promoting, [5] workers in the epilogue, [6] kernel cycles.
+  unsigned long long prof_t0 = clock64(), prof_acc = 0;
+  auto tick = [&]() { return p.prof ? clock64() : 0ull; };
   const int kblocks = p.kblocks;
   const int nchunks = (kblocks + p.chunk - 1) / p.chunk;
   const long long total_chunks = my_tiles * nchunks;
@@ -993,7 +1001,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               if (spin == 4096) sync_wait = false;
             }
           }
+          const unsigned long long w0 = tick();
           mbar_wait(&empty[s], ph ^ 1);
+          if (p.prof) prof_acc += clock64() - w0;
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
           if constexpr (kSplitA) {
             // Both CTAs' bytes complete on the leader's full[s].
@@ -1017,6 +1027,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (p.prof && lane == 0) p.prof[8 * blockIdx.x + 0] = prof_acc;
   } else if (warp == 1) {
     if (rank == 0) {
       // The whole warp runs the issue loop (warp-uniform descriptors stay
@@ -1027,13 +1038,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       for (long long q = 0; q < total_chunks; ++q) {
         const int buf = static_cast<int>(q % Cfg::NBUF);
+        const unsigned long long w0 = tick();
         mbar_wait_cluster(&acc_empty[buf], static_cast<uint32_t>(((q / Cfg::NBUF) & 1) ^ 1));
+        if (p.prof) prof_acc += clock64() - w0;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + static_cast<uint32_t>(buf * kPairBN);
         const int kb_end = min(kblocks, (c + 1) * p.chunk);
         for (int kb = c * p.chunk; kb < kb_end; ++kb) {
+          const unsigned long long f0 = tick();
           if constexpr (kSplitA) mbar_wait(&full[s], ph);
           else mbar_wait_cluster(&conv[s], ph);
+          if (p.prof && lane == 0) atomicAdd(p.prof + 8 * blockIdx.x + 2, clock64() - f0);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = smem_u32(smem + s * Cfg::STAGE_BYTES);
           // 64-K stages: SW128 planes (128-byte rows); 32-K stages: SW64 (64-byte rows, 512-byte atoms)
@@ -1066,6 +1081,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         umma2_commit_both_if(leader, &acc_full[buf]);
         if (++c == nchunks) c = 0;
       }
+      if (p.prof && lane == 0) p.prof[8 * blockIdx.x + 1] = prof_acc;
     } else if (lane == 0) {
       // Peer CTA: relay its workers' (CTA-scope, cheap) arrivals to the
       // leader's barriers.  The cluster-scope release this needs costs a
@@ -1150,6 +1166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       return static_cast<long long>((static_cast<unsigned long long>(hi) << 32) | lo);
     };
     float local = 0.f;
+    unsigned long long prof_w[3] = {0, 0, 0};
     // Raw-A stage conversion, serviced cooperatively: the same warps convert
     // the stages of chunk q and write the epilogue of chunk q - 1.  Converting
     // all of chunk q first (each stage gated by the MMA freeing a smem slot)
@@ -1206,6 +1223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (q >= 1) {
         const long long qq = q - 1;
         const int buf = static_cast<int>(qq % Cfg::NBUF);
+        const unsigned long long a0 = tick();
         if constexpr (kSplitA) {
           mbar_wait(&acc_full[buf], static_cast<uint32_t>((qq / Cfg::NBUF) & 1));
         } else {
@@ -1213,6 +1231,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             service(q, false);
         }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const unsigned long long a1 = tick();
+        if (p.prof) prof_w[0] += a1 - a0;
         if constexpr (!kDirect) {
 #pragma unroll
           for (int j = 0; j < HALF / 16; ++j) {
@@ -1238,6 +1258,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
+        const unsigned long long a2 = tick();
+        if (p.prof) prof_w[1] += a2 - a1;
         const int prev = static_cast<int>((qq + Cfg::NBUF - 1) % Cfg::NBUF);  // kDirect 3: the tile's first chunk
         // 16 accumulator columns of this lane's row straight from TMEM.
         auto tmem16 = [&](int col, float* v) {
@@ -1433,8 +1455,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int i = 0; i < HALF; ++i) acc[i] = 0.f;
           }
+          if (p.prof) prof_w[2] += clock64() - a2;
         }
       }
+    }
+    if (p.prof && warp == 2 && lane == 0) {
+      p.prof[8 * blockIdx.x + 3] = prof_w[0];
+      p.prof[8 * blockIdx.x + 4] = prof_w[1];
+      p.prof[8 * blockIdx.x + 5] = prof_w[2];
     }
     if (p.meta_c) {
       for (int o = 16; o > 0; o >>= 1) local = fmaxf(local, __shfl_xor_sync(0xffffffffu, local, o));
@@ -1447,6 +1475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync_all();
+  if (p.prof && threadIdx.x == 0) p.prof[8 * blockIdx.x + 6] = clock64() - prof_t0;
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(Cfg::TMEM_COLS));
@@ -1586,6 +1615,48 @@ CUtensorMap make_map_f16(const void* base, long long cols, long long rows, long 
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled: code " + std::to_string(r));
   return m;
+}
+
+// QSG_TC_PROF=1 (diagnostics only; synchronises after every pair launch):
+// per-CTA cycle counters of the pair kernel's roles, reported to stderr as
+// fractions of the kernel's cycles (tc_prof_report).
+unsigned long long*& tc_prof_storage() {
+  static unsigned long long* buf = nullptr;
+  return buf;
+}
+
+unsigned long long* tc_prof_buffer(cudaStream_t stream) {
+  static const bool on = std::getenv("QSG_TC_PROF") && std::getenv("QSG_TC_PROF")[0] == '1';
+  unsigned long long*& buf = tc_prof_storage();
+  if (!on) return nullptr;
+  if (!buf && cudaMalloc(&buf, 8 * sizeof(unsigned long long) * 512) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(buf, 0, 8 * sizeof(unsigned long long) * 512, stream);
+  return buf;
+}
+
+void tc_prof_report(std::int64_t m, std::int64_t n, std::int64_t k, cudaStream_t stream) {
+  unsigned long long* buf = tc_prof_storage();
+  if (!buf) return;
+  std::vector<unsigned long long> h(8 * 512);
+  cudaStreamSynchronize(stream);
+  cudaMemcpy(h.data(), buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  double sum[7] = {0, 0, 0, 0, 0, 0, 0};
+  int ctas = 0, leaders = 0;
+  for (int c = 0; c < 512; ++c) {
+    if (h[8 * c + 6] == 0) continue;
+    ++ctas;
+    const double tot = static_cast<double>(h[8 * c + 6]);
+    for (int f = 0; f < 6; ++f) sum[f] += h[8 * c + f] / tot;
+    if (h[8 * c + 2] != 0) ++leaders;
+    sum[6] += tot;
+  }
+  if (ctas == 0) return;
+  std::fprintf(stderr,
+               "qsg-prof m=%lld n=%lld k=%lld ctas=%d cycles=%.3g | producer wait-free-stage %.1f%% | MMA wait-TMEM "
+               "%.1f%% wait-stage %.1f%% | workers wait-acc %.1f%% promote %.1f%% epilogue %.1f%%\n",
+               static_cast<long long>(m), static_cast<long long>(n), static_cast<long long>(k), ctas, sum[6] / ctas,
+               100 * sum[0] / ctas, 100 * sum[1] / std::max(leaders, 1), 100 * sum[2] / std::max(leaders, 1),
+               100 * sum[3] / ctas, 100 * sum[4] / ctas, 100 * sum[5] / ctas);
 }
 
 int env_int(const char* name, int dflt) {
@@ -1764,6 +1835,7 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.c_total = g.m * g.n;
   p.stream_store = std::getenv("QSG_TC_STCS") && std::getenv("QSG_TC_STCS")[0] == '0' ? 0 : 1;  // measured ~2% on config 2
   p.passes = env_int("QSG_TC_PASSES", 3) == 2 ? 2 : 3;  // 2: inaccurate, measures MMA-count vs power only
+  p.prof = tc_prof_buffer(stream);
   p.convert_ahead = std::getenv("QSG_TC_SERVICE") && std::getenv("QSG_TC_SERVICE")[0] == '0' ? 1 : 0;
   p.meta_a = meta_a;
   p.meta_b = meta_b;
@@ -2213,6 +2285,7 @@ cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches) {
       default: e = launch_f16_pair<32>(g, ma, mb, bhi, blo, sync, ahi, alo, stream); break;
     }
     if (launches) ++*launches;
+    tc_prof_report(g.m, g.n, g.k, stream);
     return e;
   }
   float* bhi = static_cast<float*>(g.workspace);
