@@ -106,6 +106,7 @@ struct TcParams {
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int passes;         // fp16 kernel: 3 (hi.hi + hi.lo + lo.hi); 2 = power-model experiment only (QSG_TC_PASSES)
   unsigned long long* prof;  // fp16 pair kernel, QSG_TC_PROF=1: per-CTA role wait / busy cycle counters
+  int prefetch;       // fp16 kernel, pre-split A: L2-prefetch the A boxes this many k-blocks ahead
   int convert_ahead;  // fp16 kernel, raw A: convert a chunk's stages before the previous chunk's epilogue (A/B knob)
   int store_perm, nrow_bits, ncol_bits;  // fused output permutation (see GemmArgs)
   unsigned char row_pos[48];
@@ -167,6 +168,12 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       "[%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(bar), "r"(x), "r"(y)
       : "memory");
+}
+
+// L2 prefetch of a tensor-map box (no shared memory, no barrier).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(x), "r"(y)
+               : "memory");
 }
 
 // K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms
@@ -1006,6 +1013,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (p.prof) prof_acc += clock64() - w0;
           uint8_t* st = smem + s * Cfg::STAGE_BYTES;
           if constexpr (kSplitA) {
+            // A streams from HBM with only STAGES boxes in flight per CTA
+            // (the loop measured latency-bound: producer and MMA both
+            // waiting, QSG_TC_PROF); prefetch the A boxes `prefetch`
+            // k-blocks ahead into L2 so the stage loads hit L2.
+            if (p.prefetch > 0) {
+              const long long gp = gk + p.prefetch;
+              const long long tp = gp / kblocks;
+              if (tp < my_tiles) {
+                long long mp_pair;
+                int np_tile;
+                pair_tile_coords(cluster + tp * nclusters, m_pairs, p.n_tiles, mp_pair, np_tile, p.group_m);
+                const int prow = static_cast<int>(mp_pair * 256 + static_cast<long long>(rank) * BM);
+                const int pk = static_cast<int>(gp % kblocks) * kBK;
+                tma_prefetch_2d(&map_a, pk, prow);
+                tma_prefetch_2d(&map_alo, pk, prow);
+              }
+            }
             // Both CTAs' bytes complete on the leader's full[s].
             uint32_t bar = smem_u32(&full[s]);
             if (rank == 0) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
@@ -1836,6 +1860,7 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.stream_store = std::getenv("QSG_TC_STCS") && std::getenv("QSG_TC_STCS")[0] == '0' ? 0 : 1;  // measured ~2% on config 2
   p.passes = env_int("QSG_TC_PASSES", 3) == 2 ? 2 : 3;  // 2: inaccurate, measures MMA-count vs power only
   p.prof = tc_prof_buffer(stream);
+  p.prefetch = env_int("QSG_TC_PREFETCH", 0) > 0 ? env_int("QSG_TC_PREFETCH", 0) : 0;
   p.convert_ahead = std::getenv("QSG_TC_SERVICE") && std::getenv("QSG_TC_SERVICE")[0] == '0' ? 1 : 0;
   p.meta_a = meta_a;
   p.meta_b = meta_b;
