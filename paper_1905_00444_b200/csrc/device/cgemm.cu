@@ -69,6 +69,10 @@ __device__ __forceinline__ void block_max_to_meta(float local, TMeta* meta) {
   }
 }
 
+// Output column of accumulator j (0..7) of thread column tx (0..15):
+// pairs 2 tx + 32 (j / 2) + (j % 2), so each B / C access is a 16-byte pair.
+__device__ __forceinline__ int simt_col(int tx, int j) { return 2 * tx + 32 * (j >> 1) + (j & 1); }
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(NT, 2) cgemm_simt_kernel(const KParams p) {
   __shared__ __align__(16) float2 As[2][BK][BM + 2];
@@ -133,9 +137,15 @@ __global__ void __launch_bounds__(NT, 2) cgemm_simt_kernel(const KParams p) {
       const float4 a23 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4 + 2]);
       const float2 av[4] = {make_float2(a01.x, a01.y), make_float2(a01.z, a01.w), make_float2(a23.x, a23.y),
                             make_float2(a23.z, a23.w)};
+      // Thread tx owns column pairs 2 tx + 32 jj + {0, 1}: one 16-byte shared
+      // load per pair (4 LDS.128 instead of 8 LDS.64 per k).
       float2 bv[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bv[j] = Bs[buf][kk][tx + 16 * j];
+      for (int jj = 0; jj < 4; ++jj) {
+        const float4 q = *reinterpret_cast<const float4*>(&Bs[buf][kk][2 * tx + 32 * jj]);
+        bv[2 * jj] = make_float2(q.x, q.y);
+        bv[2 * jj + 1] = make_float2(q.z, q.w);
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -154,7 +164,7 @@ __global__ void __launch_bounds__(NT, 2) cgemm_simt_kernel(const KParams p) {
       if (gm >= M) continue;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const long long gn = n0 + tx + 16 * j;
+        const long long gn = n0 + simt_col(tx, j);
         if (gn < N) out[gm * N + gn] = acc[i][j];
       }
     }
@@ -168,12 +178,23 @@ __global__ void __launch_bounds__(NT, 2) cgemm_simt_kernel(const KParams p) {
   for (int i = 0; i < 4; ++i) {
     const long long gm = m0 + ty * 4 + i;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const long long gn = n0 + tx + 16 * j;
-      if (gm < M && gn < N) {
-        const float2 v = make_float2(scalbnf(acc[i][j].x, -shift), scalbnf(acc[i][j].y, -shift));
-        p.c[gm * N + gn] = v;
-        local = fmaxf(local, v.x * v.x + v.y * v.y);
+    for (int j = 0; j < 8; j += 2) {
+      const long long gn = n0 + simt_col(tx, j);
+      if (gm >= M) continue;
+      const float2 v0 = make_float2(scalbnf(acc[i][j].x, -shift), scalbnf(acc[i][j].y, -shift));
+      const float2 v1 = make_float2(scalbnf(acc[i][j + 1].x, -shift), scalbnf(acc[i][j + 1].y, -shift));
+      if (gn + 1 < N && (N & 1) == 0) {  // the pair is adjacent and 16-byte aligned
+        *reinterpret_cast<float4*>(p.c + gm * N + gn) = make_float4(v0.x, v0.y, v1.x, v1.y);
+        local = fmaxf(local, fmaxf(v0.x * v0.x + v0.y * v0.y, v1.x * v1.x + v1.y * v1.y));
+      } else {
+        if (gn < N) {
+          p.c[gm * N + gn] = v0;
+          local = fmaxf(local, v0.x * v0.x + v0.y * v0.y);
+        }
+        if (gn + 1 < N) {
+          p.c[gm * N + gn + 1] = v1;
+          local = fmaxf(local, v1.x * v1.x + v1.y * v1.y);
+        }
       }
     }
   }
