@@ -352,22 +352,30 @@ void Engine::compile() {
 
     // Lookahead: the labels the consuming step will contract this output
     // against (its other operand's label set).
-    std::set<Label> next_con;
-    bool has_next = false;
-    for (std::size_t sj = si + 1; sj < plan_.steps.size() && !has_next; ++sj) {
-      const auto& nx = plan_.steps[sj];
-      if (nx.lhs != step.out && nx.rhs != step.out) continue;
-      const std::string& other = nx.lhs == step.out ? nx.rhs : nx.lhs;
-      auto lv = live.find(other);
-      if (lv != live.end()) {
-        next_con.insert(lv->second.labels.begin(), lv->second.labels.end());
-      } else {
-        for (std::size_t sk = 0; sk < sj; ++sk)
-          if (plan_.steps[sk].out == other)
-            next_con.insert(plan_.steps[sk].out_labels.begin(), plan_.steps[sk].out_labels.end());
+    // Lookahead: the labels the consuming step will contract this output
+    // against (its other operand's label set), and the same one step further
+    // (the consumer's consumer, for the output's row-bit order below).
+    auto consumer_of = [&](const std::string& name, std::size_t from, std::set<Label>& con) -> std::size_t {
+      for (std::size_t sj = from; sj < plan_.steps.size(); ++sj) {
+        const auto& nx = plan_.steps[sj];
+        if (nx.lhs != name && nx.rhs != name) continue;
+        const std::string& other = nx.lhs == name ? nx.rhs : nx.lhs;
+        auto lv = live.find(other);
+        if (lv != live.end()) {
+          con.insert(lv->second.labels.begin(), lv->second.labels.end());
+        } else {
+          for (std::size_t sk = 0; sk < sj; ++sk)
+            if (plan_.steps[sk].out == other)
+              con.insert(plan_.steps[sk].out_labels.begin(), plan_.steps[sk].out_labels.end());
+        }
+        return sj;
       }
-      has_next = true;
-    }
+      return plan_.steps.size();
+    };
+    std::set<Label> next_con, next2_con;
+    const std::size_t next_step = consumer_of(step.out, si + 1, next_con);
+    const bool has_next = next_step < plan_.steps.size();
+    if (has_next) consumer_of(plan_.steps[next_step].out, next_step + 1, next2_con);
     // Free labels the next step contracts go last (they become the
     // trailing bits of the output, so it is usable there without a permute).
     auto next_last = [&](std::vector<Label> v) {
@@ -498,6 +506,13 @@ void Engine::compile() {
       for (const auto& l : a_free) (next_con.count(l) ? cn : fr).push_back(l);
       std::vector<Label> cn_b;
       for (const auto& l : b_free) (next_con.count(l) ? cn_b : fr).push_back(l);
+      // Two-step lookahead (QSG_LAYOUT2=0 disables): the labels the step
+      // after next contracts become the lowest ROW bits of the next step's A,
+      // so that step's fused store puts consecutive rows into adjacent runs
+      // (its own next-contracted row labels sit right above its column run).
+      static const bool layout2 = !(std::getenv("QSG_LAYOUT2") && std::getenv("QSG_LAYOUT2")[0] == '0');
+      if (layout2)
+        std::stable_partition(fr.begin(), fr.end(), [&](const Label& l) { return next2_con.count(l) == 0; });
       std::vector<Label> cand = fr;
       cand.insert(cand.end(), cn.begin(), cn.end());
       cand.insert(cand.end(), cn_b.begin(), cn_b.end());
