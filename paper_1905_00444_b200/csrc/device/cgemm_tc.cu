@@ -99,7 +99,6 @@ struct TcParams {
   unsigned int* sync;  // fp16 kernel: K-sync arrival counters per checkpoint of the persistent run (null: off)
   int sync_every;      // k-blocks between checkpoints
   int a_presplit;      // fp16 kernel: A stored split (TMeta::split_exp), see GemmArgs
-  int a_blocked;       // fp16 kernel: pre-split A in the k-blocked layout (4-D A maps), see GemmArgs
   int c_split;         // fp16 kernel: write C split
   int log2k;           // ceil(log2(k)): the split output's bound exponent
   long long c_total;   // complex elements of C (offset of the lo plane / 4 bytes)
@@ -168,17 +167,6 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
       "[%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(bar), "r"(x), "r"(y)
-      : "memory");
-}
-
-// CTA-pair TMA of a 4-D box (the k-blocked A planes: coordinates
-// {0, 0, k-block, 128-row block}).
-__device__ __forceinline__ void tma_load_4d_pair(const CUtensorMap* map, uint32_t bar, void* dst, int x, int y, int z,
-                                                 int w) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-      "%5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z), "r"(w)
       : "memory");
 }
 
@@ -1046,13 +1034,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t bar = smem_u32(&full[s]);
             if (rank == 0) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
             else asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(bar) : "r"(bar));
-            if (p.a_blocked) {  // one contiguous 16 KiB run per plane
-              tma_load_4d_pair(&map_a, bar, st, 0, 0, kb, row0 / BM);
-              tma_load_4d_pair(&map_alo, bar, st + Cfg::A_B / 2, 0, 0, kb, row0 / BM);
-            } else {
-              tma_load_2d_pair(&map_a, bar, st, kb * kBK, row0);
-              tma_load_2d_pair(&map_alo, bar, st + Cfg::A_B / 2, kb * kBK, row0);
-            }
+            tma_load_2d_pair(&map_a, bar, st, kb * kBK, row0);
+            tma_load_2d_pair(&map_alo, bar, st + Cfg::A_B / 2, kb * kBK, row0);
             tma_load_2d_pair(&map_bhi, bar, st + Cfg::A_B, kb * kBK, brow0);
             tma_load_2d_pair(&map_blo, bar, st + Cfg::A_B + Cfg::B_B, kb * kBK, brow0);
             if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
@@ -1700,22 +1683,6 @@ void tc_prof_report(std::int64_t m, std::int64_t n, std::int64_t k, cudaStream_t
                100 * sum[3] / ctas, 100 * sum[4] / ctas, 100 * sum[5] / ctas);
 }
 
-// 4-D fp16 map of a k-blocked plane (GemmArgs::a_blocked): dims {64 real
-// K, 128 rows, k / 32 blocks, m / 128 row blocks}, box {64, 128, 1, 1}, SW128
-// -- the same shared-memory image as the 2-D box of the row-major plane.
-CUtensorMap make_map_f16_blocked(const void* base, long long k, long long m) {
-  CUtensorMap t;
-  const cuuint64_t dims[4] = {64, 128, static_cast<cuuint64_t>(k / 32), static_cast<cuuint64_t>(m / 128)};
-  const cuuint64_t strides[3] = {128, 128 * 128, static_cast<cuuint64_t>(k / 32) * 128 * 128};
-  const cuuint32_t box[4] = {64, 128, 1, 1};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode_fn()(&t, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box,
-                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, kL2Promo,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw std::runtime_error("CUDA error in cuTensorMapEncodeTiled (blocked): code " + std::to_string(r));
-  return t;
-}
-
 int env_int(const char* name, int dflt) {
   const char* env = std::getenv(name);
   const int v = env ? std::atoi(env) : dflt;
@@ -1871,14 +1838,8 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   // pre-split tiles, whose A streams from HBM (more bytes in flight).
   static const bool stage32 = env_int("QSG_TC_STAGEK", 64) == 32;
   const int kb = (split && stage32 && 2 * g.k <= 512) ? 32 : BK16;
-  if (g.a_blocked && !(split && g.a_presplit && kb == BK16))
-    throw std::invalid_argument("cgemm_tc: k-blocked A needs pre-split A and 64-K stages");
-  const CUtensorMap ma = g.a_blocked ? make_map_f16_blocked(ahi, g.k, g.m)
-                         : split     ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM, kb)
-                                     : make_map(g.a, 2 * g.k, g.m, BM);
-  const CUtensorMap mal = g.a_blocked ? make_map_f16_blocked(alo, g.k, g.m)
-                          : split     ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM, kb)
-                                      : ma;
+  const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM, kb) : make_map(g.a, 2 * g.k, g.m, BM);
+  const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM, kb) : ma;
   const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
   const CUtensorMap mbl = make_map_f16(blo, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
   TcParams p{};
@@ -1891,7 +1852,6 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.sync = sync;
   p.sync_every = sync_every();
   p.a_presplit = g.a_presplit ? 1 : 0;
-  p.a_blocked = g.a_blocked ? 1 : 0;
   p.c_split = g.c_split ? 1 : 0;
   int l2k = 0;
   while ((std::int64_t{1} << l2k) < g.k) ++l2k;
@@ -2249,13 +2209,6 @@ bool cgemm_tc_eligible(std::int64_t m, std::int64_t n, std::int64_t k, bool tran
 
 bool cgemm_tc_store_perm_supported(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {
   return cgemm_tc_supported(m, n, k, trans_a, trans_b) && use_pair(m, n) && !use_3m(m, n, k);
-}
-
-bool cgemm_tc_blocked_ok(std::int64_t m, std::int64_t n, std::int64_t k) {
-  // Pre-split fp16 pair path with 64-K stages over whole 32-complex blocks
-  // (not 3M, whose prep pass reads row-major A; not 32-K stages).
-  static const bool stage32 = env_int("QSG_TC_STAGEK", 64) == 32;
-  return use_f16(m, n, k) && !use_3m(m, n, k) && m % 256 == 0 && k % 32 == 0 && !(stage32 && 2 * k <= 512);
 }
 
 bool cgemm_tc_split_ok(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b) {

@@ -71,12 +71,6 @@ struct GemmArgs {
   // this way (no conversion pass or in-kernel conversion).
   bool c_split = false;
   bool a_presplit = false;
-  // a_blocked (with a_presplit): the A planes are k-blocked -- complex
-  // element (row, kc) at ((row >> 7) * (k / 32) + (kc >> 5)) * 4096 +
-  // (row & 127) * 32 + (kc & 31) -- so every 128-row x 32-complex stage box
-  // is one contiguous 16 KiB run per plane (the producer's fused store
-  // writes it; Engine::split_handoffs).
-  bool a_blocked = false;
 };
 std::int64_t cgemm_workspace_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
 // True when cgemm runs the narrow-N kernel (n <= 32, m >= 1024): one thread

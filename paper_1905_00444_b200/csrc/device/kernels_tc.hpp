@@ -24,8 +24,6 @@ std::int64_t cgemm_tc_workspace_bytes(std::int64_t m, std::int64_t n, std::int64
 // The fp16 CTA-pair kernel handles the shape, so C may be written split /
 // A read pre-split (GemmArgs::c_split / a_presplit).
 bool cgemm_tc_split_ok(std::int64_t m, std::int64_t n, std::int64_t k, bool trans_a, bool trans_b);
-// The consumer can read pre-split A in the k-blocked layout (GemmArgs::a_blocked).
-bool cgemm_tc_blocked_ok(std::int64_t m, std::int64_t n, std::int64_t k);
 cudaError_t cgemm_tc(const GemmArgs& g, cudaStream_t stream, int* launches = nullptr);
 // Planning model of the tensor-core path for a shape: sustained Eq.(1)
 // flop/s and the HBM bytes of its operand preparation passes (B expansion,

@@ -622,42 +622,6 @@ void Engine::split_handoffs() {
       continue;
     pr.c_split = true;
     co.a_presplit = true;
-    // k-blocked A (QSG_ABLOCK=0 disables): the producer's fused store
-    // writes the consumer's stage boxes as contiguous 16 KiB runs.  In the
-    // consumer's row-major [m][k] the address bits are K (log2 k) then M;
-    // the blocked order is K_lo (5) | M_lo (7) | K_hi | M_hi, a fixed remap
-    // of the producer's output bit positions.
-    static const bool ablock = !(std::getenv("QSG_ABLOCK") && std::getenv("QSG_ABLOCK")[0] == '0');
-    int lk = 0, lm = 0;
-    while ((std::int64_t{1} << lk) < co.k) ++lk;
-    while ((std::int64_t{1} << lm) < co.m) ++lm;
-    if (ablock && (std::int64_t{1} << lk) == co.k && (std::int64_t{1} << lm) == co.m && lk >= 5 && lm >= 8 &&
-        dev::cgemm_tc_blocked_ok(co.m, co.n, co.k) &&
-        (pr.store_perm || dev::cgemm_tc_store_perm_supported(pr.m, pr.n, pr.k, pr.ta, pr.tb))) {
-      int nb = 0, cb = 0;
-      while ((std::int64_t{1} << nb) < pr.m) ++nb;
-      while ((std::int64_t{1} << cb) < pr.n) ++cb;
-      if (!pr.store_perm && (std::int64_t{1} << nb) == pr.m && (std::int64_t{1} << cb) == pr.n && cb >= 3) {
-        pr.store_perm = true;  // natural [m][n] order as an explicit permutation
-        pr.nrow_bits = nb;
-        pr.ncol_bits = cb;
-        for (int b = 0; b < nb; ++b) pr.row_pos[static_cast<std::size_t>(b)] = static_cast<unsigned char>(cb + b);
-        for (int b = 0; b < cb; ++b) pr.col_pos[static_cast<std::size_t>(b)] = static_cast<unsigned char>(b);
-      }
-      if (pr.store_perm) {
-        auto remap = [&](int b) {
-          if (b < 5) return b;               // K_lo
-          if (b < lk) return b + 7;          // K_hi above M_lo
-          if (b < lk + 7) return b - lk + 5; // M_lo
-          return b;                          // M_hi
-        };
-        for (int b = 0; b < pr.nrow_bits; ++b)
-          pr.row_pos[static_cast<std::size_t>(b)] = static_cast<unsigned char>(remap(pr.row_pos[static_cast<std::size_t>(b)]));
-        for (int b = 0; b < pr.ncol_bits; ++b)
-          pr.col_pos[static_cast<std::size_t>(b)] = static_cast<unsigned char>(remap(pr.col_pos[static_cast<std::size_t>(b)]));
-        co.a_blocked = true;
-      }
-    }
     co.ws_bytes = dev::cgemm_tc_workspace_bytes(co.m, co.n, co.k, co.ta, co.tb, true);
     if (co.ws >= 0) bufs_[static_cast<std::size_t>(co.ws)].bytes = align_up(std::max<std::int64_t>(co.ws_bytes, 8));
   }
@@ -939,7 +903,6 @@ void Engine::launch_op(std::size_t i, const std::vector<std::int64_t>& node_off,
     g.store_perm = op.store_perm;
     g.c_split = op.c_split;
     g.a_presplit = op.a_presplit;
-    g.a_blocked = op.a_blocked;
     g.nrow_bits = op.nrow_bits;
     g.ncol_bits = op.ncol_bits;
     std::copy(op.row_pos.begin(), op.row_pos.end(), g.row_pos);
@@ -1200,7 +1163,7 @@ std::string Engine::describe() const {
          << (op.ta ? " TA" : "") << (op.tb ? " TB" : "") << (op.tc ? " tc" : " simt") << " ws " << op.ws_bytes
          << (op.store_perm ? " fused-store" : "") << (op.store_perm ? perm_text(op) : std::string())
          << (op.c_split ? " split-out" : "")
-         << (op.a_presplit ? " split-in" : "") << (op.a_blocked ? " blocked-in" : "")
+         << (op.a_presplit ? " split-in" : "")
          << (op.ooc ? " ooc pieces " + std::to_string(op.pieces.size()) : std::string()) << "\n";
     else os << "  accumulate " << op.count << "\n";
   }

@@ -161,7 +161,6 @@ class Engine {
     std::array<unsigned char, 24> col_pos{};
     bool c_split = false;     // C written as fp16 hi | lo planes (dev::GemmArgs::c_split)
     bool a_presplit = false;  // A read as fp16 hi | lo planes
-    bool a_blocked = false;   // ... in the k-blocked layout (dev::GemmArgs::a_blocked)
     // Out-of-core GEMM: m / n row-column blocks (m0, mp, n0, np) streamed
     // through the device pipeline; C in host memory.
     bool ooc = false;
