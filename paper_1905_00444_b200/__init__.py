@@ -16,7 +16,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqsg.so")
+LIB_PATH = os.environ.get("QSG_LIB") or os.path.join(_HERE, "libqsg.so")  # QSG_LIB: A/B builds only
 
 __all__ = [
     "QsgError", "CircuitError", "lib", "mix_seed", "flop_count", "generate_rqc", "canonical_circuit",

@@ -103,6 +103,7 @@ struct TcParams {
   int log2k;           // ceil(log2(k)): the split output's bound exponent
   long long c_total;   // complex elements of C (offset of the lo plane / 4 bytes)
   int stream_store;    // fp16 kernel: evict-first (st.global.cs) output stores
+  int lane_store;      // host only: launch the kLane instantiation (split output, lane = row STG.256)
   int half_tail;  // fp16 kernel: the last k-block has only its first 32 real K (2k % 64 == 32)
   int passes;         // fp16 kernel: 3 (hi.hi + hi.lo + lo.hi); 2 = power-model experiment only (QSG_TC_PASSES)
   unsigned long long* prof;  // fp16 pair kernel, QSG_TC_PROF=1: per-CTA role wait / busy cycle counters
@@ -178,6 +179,18 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, i
 
 // K-major, SWIZZLE_128B smem matrix descriptor (rows of 128 B, 8-row atoms
 // of 1024 B; SBO = 1024 B; version 1; layout type 2 = SWIZZLE_128B).
+// One 32-byte (full sector) store per lane: STG.256 (sm_100), evict-first or not.
+__device__ __forceinline__ void st_global_v8(void* g, const uint32_t* v, bool evict_first) {
+  if (evict_first)
+    asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(g), "r"(v[0]), "r"(v[1]),
+                 "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+  else
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(g), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 __device__ __forceinline__ uint64_t kmajor_sw128_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
@@ -896,7 +909,7 @@ struct Tc5Cfg {
 // accumulator buffer after the tile's stores (the MMA meanwhile fills the
 // other buffer).  Without the 128 promoted floats per thread the worker
 // warps run spill-free.
-template <int kPairBN, bool kSplitA, int kBK = BK16, int kDirect = 0>
+template <int kPairBN, bool kSplitA, int kBK = BK16, int kDirect = 0, bool kLane = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cgemm_f16_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_alo,
                           const __grid_constant__ CUtensorMap map_bhi, const __grid_constant__ CUtensorMap map_blo,
@@ -1319,8 +1332,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           // The rows' offsets, read back per store (no shuffles, no registers).
           if (p.store_perm) row_tab[lane] = static_cast<uint32_t>((my_row_off + col_tile_off) >> 3);
           bool stored = false;
+          if constexpr (kLane) {
+            static_assert((kDirect == 0 || kDirect == 1) && HALF >= 16, "lane stores: promoted or direct tiles");
+            {
+              // Split output, lane = row, no staging: every 8 complex of the
+              // lane's row are one 32-byte run per plane (complex column
+              // bits 0..2 are the output's bits 0..2 under the fused
+              // permutation; natural order needs n % 8 == 0), written as one
+              // STG.256 per plane straight from registers (its own
+              // instantiation: the staged paths' registers stay out).  The max is kept
+              // on the split values y = acc * 2^-t and rescaled once per tile
+              // (an exact power of two).
+              const long long row_off =
+                  p.store_perm ? my_row_off + col_tile_off
+                               : (row_base + lane) * (p.n2 / 2) + (static_cast<long long>(n_tile) * kPairBN + half * HALF) / 2;
+              float ymax = 0.f;
+#pragma unroll
+              for (int g = 0; g < HALF / 16; ++g) {
+                if ((g & 1) == 0) service(q, false);
+                float a16[16];
+                if constexpr (kFromTmem) {
+                  tmem16(16 * g, a16);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 16; ++i) a16[i] = acc[16 * g + i];
+                }
+                uint32_t hh[8], ll[8];
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                  const float y0 = a16[2 * t] * fy, y1 = a16[2 * t + 1] * fy;
+                  ymax = fmaxf(ymax, y0 * y0 + y1 * y1);
+                  const __half2 h = __floats2half2_rn(y0, y1);
+                  const float2 g2 = __half22float2(h);
+                  hh[t] = h2_bits(h);
+                  ll[t] = h2_bits(__floats2half2_rn(y0 - g2.x, y1 - g2.y));
+                }
+                const long long o =
+                    row_off + (p.store_perm ? ((g & 1) ? col_bit(3) : 0ll) + ((g & 2) ? col_bit(4) : 0ll) +
+                                                  ((g & 4) ? col_bit(5) : 0ll)
+                                            : 8ll * g);
+                st_global_v8(c_bytes + 4 * o, hh, p.stream_store != 0);
+                st_global_v8(c_bytes + lo_plane + 4 * o, ll, p.stream_store != 0);
+              }
+              local = fmaxf(local, scalbnf(ymax, 2 * (t_split - unscale)));
+              stored = true;
+            }
+          }
           if constexpr (HALF >= 32 && kDirect) {
-            if (p.c_split) {
+            if (p.c_split && !stored) {
               // Split output in 32-column slabs: lane = row stages 32 floats
               // (chunk c of row r at 16-byte slot c ^ (r & 7): conflict-free
               // both ways), then 4 lanes per row convert 4 complex each and
@@ -1858,6 +1917,16 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   p.log2k = l2k;
   p.c_total = g.m * g.n;
   p.stream_store = std::getenv("QSG_TC_STCS") && std::getenv("QSG_TC_STCS")[0] == '0' ? 0 : 1;  // measured ~2% on config 2
+  {
+    // Lane-per-row split stores (QSG_TC_LANESTORE=0: the staged slab paths):
+    // 32-byte aligned planes and 8-complex runs per row.
+    const char* ls = std::getenv("QSG_TC_LANESTORE");
+    const bool on = !(ls && ls[0] == '0');
+    p.lane_store = on && g.c_split && reinterpret_cast<std::uintptr_t>(g.c) % 32 == 0 && p.c_total % 8 == 0 &&
+                           (g.store_perm || g.n % 8 == 0)
+                       ? 1
+                       : 0;
+  }
   p.passes = env_int("QSG_TC_PASSES", 3) == 2 ? 2 : 3;  // 2: inaccurate, measures MMA-count vs power only
   p.prof = tc_prof_buffer(stream);
   p.prefetch = env_int("QSG_TC_PREFETCH", 0) > 0 ? env_int("QSG_TC_PREFETCH", 0) : 0;
@@ -1952,6 +2021,29 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
         cgemm_f16_pair_kernel<BN, false, BK16, 3><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
       return cudaGetLastError();
     }
+  }
+  if (p.lane_store && !(direct && early)) {
+    static const bool attrs_lane = [] {
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Tc5Cfg<BN>::SMEM);
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, 0, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg<BN>::SMEM);
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, BK16, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           Tc5Cfg<BN>::SMEM);
+      cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false, BK16, 1, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, Tc5Cfg<BN>::SMEM);
+      return true;
+    }();
+    (void)attrs_lane;
+    if (direct && split)
+      cgemm_f16_pair_kernel<BN, true, BK16, 1, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    else if (direct)
+      cgemm_f16_pair_kernel<BN, false, BK16, 1, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    else if (split)
+      cgemm_f16_pair_kernel<BN, true, BK16, 0, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    else
+      cgemm_f16_pair_kernel<BN, false, BK16, 0, true><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+    return cudaGetLastError();
   }
   if (direct && split && early)
     cgemm_f16_pair_kernel<BN, true, BK16, 2><<<grid, kThreads, Tc5Cfg<BN>::SMEM, stream>>>(ma, mal, mbh, mbl, p);

@@ -21,8 +21,11 @@ def main():
     if variant:  # index among all `name` launches (ncu -k regex:name -s IDX), longest of one template variant
         names = [x["Kernel Name"] for x in rs if name in x["Kernel Name"]]
         cand = [(i, v) for i, v in hits if variant[0] in names[i]]
-        top = max(v for _, v in cand)
-        print(min(i for i, v in cand if v >= 0.95 * top))
+        if len(rng) == 2:  # --ms window too: the first launch of the variant inside it
+            print(min(i for i, v in cand if rng[0] <= v <= rng[1]))
+        else:
+            top = max(v for _, v in cand)
+            print(min(i for i, v in cand if v >= 0.95 * top))
     elif len(rng) == 2:
         print(min(i for i, v in hits if rng[0] <= v <= rng[1]))  # first launch in the duration window
     else:
