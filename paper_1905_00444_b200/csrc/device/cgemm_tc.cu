@@ -2107,6 +2107,10 @@ __device__ __forceinline__ void split16(float x, __half& hi, __half& lo) {
 // A (complex [m][k]: raw fp32, or split fp16 hi | lo planes of the 2x2 path
 // with value (hi + lo) 2^-split_exp) -> Ar, Ai, S = Ar + Ai, each as fp16
 // hi | lo planes [m][k] scaled by 2^(f16_exp(meta) - 1).
+__device__ __forceinline__ uint32_t pack_h2(__half lo, __half hi) {
+  return static_cast<uint32_t>(__half_as_ushort(lo)) | (static_cast<uint32_t>(__half_as_ushort(hi)) << 16);
+}
+
 __global__ void __launch_bounds__(256) tc3m_prep_a_kernel(const void* __restrict__ a, int presplit,
                                                           long long count, const TMeta* __restrict__ meta,
                                                           __half* __restrict__ planes, TMeta* __restrict__ scratch) {
@@ -2119,7 +2123,59 @@ __global__ void __launch_bounds__(256) tc3m_prep_a_kernel(const void* __restrict
   __half* const ail = aih + count;
   __half* const ssh = ail + count;
   __half* const ssl = ssh + count;
-  for (long long i = blockIdx.x * 256ll + threadIdx.x; i < count; i += static_cast<long long>(gridDim.x) * 256) {
+  const long long stride = static_cast<long long>(gridDim.x) * 256;
+  // 8 complex per thread and pass: 2 x 32-byte reads, 6 x 16-byte plane
+  // writes (count % 8 == 0 keeps every plane 16-byte aligned); the element
+  // arithmetic is the scalar tail's.
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(planes)) & 15) == 0;
+  const long long n8 = count % 8 == 0 && aligned ? count / 8 : 0;
+  for (long long v = blockIdx.x * 256ll + threadIdx.x; v < n8; v += stride) {
+    float re[8], im[8];
+    if (presplit) {
+      const uint4* hp = reinterpret_cast<const uint4*>(a) + 2 * v;
+      const uint4* lp = reinterpret_cast<const uint4*>(reinterpret_cast<const __half2*>(a) + count) + 2 * v;
+      const uint4 hw[2] = {__ldcs(hp), __ldcs(hp + 1)}, lw[2] = {__ldcs(lp), __ldcs(lp + 1)};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t hs[4] = {hw[q].x, hw[q].y, hw[q].z, hw[q].w}, ls[4] = {lw[q].x, lw[q].y, lw[q].z, lw[q].w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const __half2 h = *reinterpret_cast<const __half2*>(&hs[t]), l = *reinterpret_cast<const __half2*>(&ls[t]);
+          re[4 * q + t] = __low2float(h) + __low2float(l);
+          im[4 * q + t] = __high2float(h) + __high2float(l);
+        }
+      }
+    } else {
+      const float4* fp = reinterpret_cast<const float4*>(a) + 4 * v;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 f = __ldcs(fp + q);
+        re[2 * q] = f.x;
+        im[2 * q] = f.y;
+        re[2 * q + 1] = f.z;
+        im[2 * q + 1] = f.w;
+      }
+    }
+    uint32_t w[6][4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      __half h[6][2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float r = re[2 * t + u] * s, m = im[2 * t + u] * s;
+        split16(r, h[0][u], h[1][u]);
+        split16(m, h[2][u], h[3][u]);
+        split16(r + m, h[4][u], h[5][u]);
+      }
+#pragma unroll
+      for (int pl = 0; pl < 6; ++pl) w[pl][t] = pack_h2(h[pl][0], h[pl][1]);
+    }
+    __half* const dst[6] = {arh, arl, aih, ail, ssh, ssl};
+#pragma unroll
+    for (int pl = 0; pl < 6; ++pl)
+      __stcs(reinterpret_cast<uint4*>(dst[pl]) + v, make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]));
+  }
+  for (long long i = 8 * n8 + blockIdx.x * 256ll + threadIdx.x; i < count; i += stride) {
     float re, im;
     if (presplit) {
       const __half2 h = reinterpret_cast<const __half2*>(a)[i];
@@ -2140,33 +2196,66 @@ __global__ void __launch_bounds__(256) tc3m_prep_a_kernel(const void* __restrict
 }
 
 // B (complex [k][n], or [n][k] when tb) -> B^T real planes [n][k]: Br, Bi,
-// T = Br + Bi, each fp16 hi | lo scaled by 2^(f16_exp(meta) - 1).
+// T = Br + Bi, each fp16 hi | lo scaled by 2^(f16_exp(meta) - 1).  Tiles of
+// 128 k x 32 n through shared memory (stored [n][k]); every lane then writes
+// 4 consecutive k (8 bytes) per plane, a warp one 256-byte run of one n row.
 __global__ void __launch_bounds__(256) tc3m_prep_b_kernel(const float2* __restrict__ b, long long n, long long k,
                                                           int tb, const TMeta* __restrict__ meta,
                                                           __half* __restrict__ planes) {
-  __shared__ float2 tile[32][33];
-  const long long j0 = static_cast<long long>(blockIdx.x) * 32, p0 = static_cast<long long>(blockIdx.y) * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int r = ty; r < 32; r += 8) {
-    if (!tb) {
-      const long long p = p0 + r, j = j0 + tx;
-      tile[r][tx] = (p < k && j < n) ? b[p * n + j] : make_float2(0.f, 0.f);
-    } else {
-      const long long j = j0 + r, p = p0 + tx;
-      tile[tx][r] = (p < k && j < n) ? b[j * k + p] : make_float2(0.f, 0.f);
+  constexpr int TK = 128, TN = 32, PITCH = TK + 1;
+  __shared__ float2 tile[TN][PITCH];
+  const long long j0 = static_cast<long long>(blockIdx.x) * TN, p0 = static_cast<long long>(blockIdx.y) * TK;
+  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+  if (!tb) {
+    for (int r = wy; r < TK; r += 8) {  // row p of B [k][n]: lanes over n
+      const long long p = p0 + r, j = j0 + lane;
+      tile[lane][r] = (p < k && j < n) ? b[p * n + j] : make_float2(0.f, 0.f);
+    }
+  } else {
+    for (int r = wy; r < TN; r += 8) {  // row j of B^T [n][k]: lanes over k
+      const long long j = j0 + r;
+#pragma unroll
+      for (int c = 0; c < TK / 32; ++c) {
+        const long long p = p0 + 32 * c + lane;
+        tile[r][32 * c + lane] = (p < k && j < n) ? b[j * k + p] : make_float2(0.f, 0.f);
+      }
     }
   }
   __syncthreads();
   const float s = scalbnf(1.f, f16_exp_3m(meta));
   const long long nk = n * k;
-  for (int r = ty; r < 32; r += 8) {
-    const long long j = j0 + r, p = p0 + tx;
+  const bool vec = k % 4 == 0 && (reinterpret_cast<uintptr_t>(planes) & 7) == 0;
+  for (int r = wy; r < TN; r += 8) {
+    const long long j = j0 + r, p = p0 + 4 * lane;
     if (j >= n || p >= k) continue;
-    const float2 v = tile[tx][r];
-    const long long o = j * k + p;
-    split16(v.x * s, planes[o], planes[nk + o]);
-    split16(v.y * s, planes[2 * nk + o], planes[3 * nk + o]);
-    split16((v.x + v.y) * s, planes[4 * nk + o], planes[5 * nk + o]);
+    if (vec) {  // p .. p + 3 all < k (k % 4 == 0, p % 4 == 0)
+      uint32_t w[6][2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        __half h[6][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const float2 v = tile[r][4 * lane + 2 * t + u];
+          split16(v.x * s, h[0][u], h[1][u]);
+          split16(v.y * s, h[2][u], h[3][u]);
+          split16((v.x + v.y) * s, h[4][u], h[5][u]);
+        }
+#pragma unroll
+        for (int pl = 0; pl < 6; ++pl) w[pl][t] = pack_h2(h[pl][0], h[pl][1]);
+      }
+      const long long o = j * k + p;
+#pragma unroll
+      for (int pl = 0; pl < 6; ++pl)
+        *reinterpret_cast<uint2*>(planes + pl * nk + o) = make_uint2(w[pl][0], w[pl][1]);
+    } else {
+      for (int u = 0; u < 4 && p + u < k; ++u) {
+        const float2 v = tile[r][4 * lane + u];
+        const long long o = j * k + p + u;
+        split16(v.x * s, planes[o], planes[nk + o]);
+        split16(v.y * s, planes[2 * nk + o], planes[3 * nk + o]);
+        split16((v.x + v.y) * s, planes[4 * nk + o], planes[5 * nk + o]);
+      }
+    }
   }
 }
 
@@ -2231,9 +2320,10 @@ cudaError_t cgemm_tc_3m(const GemmArgs& g, const TMeta* ma, const TMeta* mb, cud
   cudaError_t e = cudaMemcpyAsync(meta_b3, mb, sizeof(TMeta), cudaMemcpyDeviceToDevice, stream);
   if (e != cudaSuccess) return e;
   {
-    const int blocks = static_cast<int>(std::min<long long>((mk + 255) / 256, 148 * 16));
+    const long long items = mk % 8 == 0 ? mk / 8 : mk;
+    const int blocks = static_cast<int>(std::min<long long>((items + 255) / 256, 148 * 16));
     tc3m_prep_a_kernel<<<blocks, 256, 0, stream>>>(g.a, g.a_presplit ? 1 : 0, mk, ma, ap, meta_a3);
-    dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 31) / 32));
+    dim3 grid(static_cast<unsigned>((g.n + 31) / 32), static_cast<unsigned>((g.k + 127) / 128));
     tc3m_prep_b_kernel<<<grid, 256, 0, stream>>>(static_cast<const float2*>(g.b), g.n, g.k, g.trans_b ? 1 : 0, mb, bp);
     tc3m_scale_meta_kernel<<<1, 1, 0, stream>>>(meta_b3);
     if (launches) *launches += 3;
