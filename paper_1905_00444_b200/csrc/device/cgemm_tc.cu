@@ -525,10 +525,12 @@ __host__ __device__ constexpr uint32_t tf32_idesc_pair() {
 // re-read all of B_r^T from HBM per wave of m tiles: 1.2 TB per s026 launch).
 __device__ __forceinline__ void pair_tile_coords(long long t, long long m_pairs, int n_tiles, long long& m_pair,
                                                  int& n_tile, int group_m = kGroupM) {
-  const long long span = static_cast<long long>(group_m) * n_tiles;
-  const long long first_m = (t / span) * group_m;
-  const long long gsize = min(static_cast<long long>(group_m), m_pairs - first_m);
-  const long long within = t % span;
+  // 32-bit divisions (64-bit ones cost ~3x on the workers' per-tile path):
+  // a launch has < 2^31 tiles (C would be > 2^47 bytes otherwise).
+  const unsigned span = static_cast<unsigned>(group_m) * static_cast<unsigned>(n_tiles), tt = static_cast<unsigned>(t);
+  const unsigned first_m = (tt / span) * static_cast<unsigned>(group_m);
+  const unsigned gsize = min(static_cast<unsigned>(group_m), static_cast<unsigned>(m_pairs) - first_m);
+  const unsigned within = tt % span;
   m_pair = first_m + within % gsize;
   n_tile = static_cast<int>(within / gsize);
 }
@@ -1837,6 +1839,7 @@ cudaError_t launch_pair(const GemmArgs& g, const float* bhi, const float* blo, c
   std::memcpy(p.row_pos, g.row_pos, sizeof p.row_pos);
   std::memcpy(p.col_pos, g.col_pos, sizeof p.col_pos);
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
+  if (pairs >= (1ll << 31)) return cudaErrorInvalidValue;  // pair_tile_coords divides in 32 bits
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
   static const long long slots = [] {
     cudaFuncSetAttribute(cgemm_tc2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Tc2Cfg<BN>::SMEM);
@@ -1896,7 +1899,9 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   // lookahead.  QSG_TC_STAGEK=32 selects them for short-K (k <= 256)
   // pre-split tiles, whose A streams from HBM (more bytes in flight).
   static const bool stage32 = env_int("QSG_TC_STAGEK", 64) == 32;
-  const int kb = (split && stage32 && 2 * g.k <= 512) ? 32 : BK16;
+  // k <= 16 (one 32-K block): 32-K stages always -- a 64-K box would stage
+  // half zero-fill and twice the L2 reads (the m = 2^27 bond-closing steps).
+  const int kb = (split && ((stage32 && 2 * g.k <= 512) || 2 * g.k <= 32)) ? 32 : BK16;
   const CUtensorMap ma = split ? make_map_f16(ahi, 2 * g.k, g.m, 2 * g.k, BM, kb) : make_map(g.a, 2 * g.k, g.m, BM);
   const CUtensorMap mal = split ? make_map_f16(alo, 2 * g.k, g.m, 2 * g.k, BM, kb) : ma;
   const CUtensorMap mbh = make_map_f16(bhi, 2 * g.k, 2 * g.n, b16_pitch(g.k), BN / 2, kb);
@@ -1961,6 +1966,7 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   std::memcpy(p.row_pos, g.row_pos, sizeof p.row_pos);
   std::memcpy(p.col_pos, g.col_pos, sizeof p.col_pos);
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
+  if (pairs >= (1ll << 31)) return cudaErrorInvalidValue;  // pair_tile_coords divides in 32 bits
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
   static const long long slots = [] {
     cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2005,6 +2011,21 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
       return true;
     }();
     (void)attrs32;
+    if (p.lane_store) {
+      static const bool attrs32l = [] {
+        cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, 32, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Tc5Cfg<BN, 32>::SMEM);
+        cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, true, 32, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Tc5Cfg<BN, 32>::SMEM);
+        return true;
+      }();
+      (void)attrs32l;
+      if (direct)
+        cgemm_f16_pair_kernel<BN, true, 32, 1, true><<<grid, kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+      else
+        cgemm_f16_pair_kernel<BN, true, 32, 0, true><<<grid, kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
+      return cudaGetLastError();
+    }
     if (direct)
       cgemm_f16_pair_kernel<BN, true, 32, 1><<<grid, kThreads, Tc5Cfg<BN, 32>::SMEM, stream>>>(ma, mal, mbh, mbl, p);
     else
