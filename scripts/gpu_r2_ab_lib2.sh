@@ -5,7 +5,7 @@ mkdir -p gpurun_out/abn
 for r in 1 2; do
   for v in "QSG_LIB=$PWD/ab/libqsg_base.so" "QSG_LIB=$PWD/paper_1905_00444_b200/libqsg.so"; do
     tag=$(basename ${v#QSG_LIB=} .so)
-    for c in 4 3 2; do
+    for c in 4 3 2 5; do
       env $v python bench.py --config $c --steps 3 --warmup 2 --no-cpu-baseline --profile-out gpurun_out/abn/ops_c${c}_${tag}_$r.jsonl > gpurun_out/abn/bench_c${c}_${tag}_$r.log 2>&1
       echo "$tag run $r c$c: $(tail -1 gpurun_out/abn/bench_c${c}_${tag}_$r.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["ms_per_step"],2), "ms/step", d["clocks"]["sm_mhz"], "MHz")') $(python scripts/prof_classes.py gpurun_out/abn/ops_c${c}_${tag}_$r.jsonl | sed -n 2,3p | tr -s ' ' | tr '\n' '|')"
     done

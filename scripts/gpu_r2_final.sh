@@ -17,3 +17,9 @@ IDX=$(python scripts/ncu_pick.py gpurun_out/final/ncu_launches_c5.csv cgemm_f16_
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cgemm_f16_pair_kernel -s $IDX -c 1 -o gpurun_out/final/ncu_full_c5_cube $CMD > gpurun_out/final/ncu_full.log 2>&1; echo "ncu rc=$?"
 # config 1: per-launch durations of one widened contraction (latency floor evidence)
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/final/ncu_launches_c1.csv python bench.py --config 1 --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/final/ncu_c1.log 2>&1; echo "ncu c1 rc=$?"
+# config 4 (Bristlecone-70): --set full of its dominant class, the k = n = 256 lane-store launch
+# (m = 2^23; --skip=1 passes over the first 7-9 ms launch of the variant, the n = 2048 step)
+C4="python bench.py --config 4 --steps 1 --warmup 0 --no-cpu-baseline"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final/ncu_launches_c4.csv $C4 > gpurun_out/final/ncu_list_c4.log 2>&1; echo "ncu list c4 rc=$?"
+IDX4=$(python scripts/ncu_pick.py gpurun_out/final/ncu_launches_c4.csv cgemm_f16_pair_kernel "--variant=cgemm_f16_pair_kernel<256, 1, 64, 0, 1>" --ms=7.0 --ms=9.0 --skip=1 --summary 2> gpurun_out/final/ncu_launches_c4_summary.txt); echo "idx4=$IDX4"; head -6 gpurun_out/final/ncu_launches_c4_summary.txt
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cgemm_f16_pair_kernel -s $IDX4 -c 1 -o gpurun_out/final/ncu_full_c4_k256 $C4 > gpurun_out/final/ncu_full_c4.log 2>&1; echo "ncu c4 rc=$?"

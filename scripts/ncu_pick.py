@@ -21,8 +21,9 @@ def main():
     if variant:  # index among all `name` launches (ncu -k regex:name -s IDX), longest of one template variant
         names = [x["Kernel Name"] for x in rs if name in x["Kernel Name"]]
         cand = [(i, v) for i, v in hits if variant[0] in names[i]]
-        if len(rng) == 2:  # --ms window too: the first launch of the variant inside it
-            print(min(i for i, v in cand if rng[0] <= v <= rng[1]))
+        if len(rng) == 2:  # --ms window too: the first launch of the variant inside it (after --skip=N others)
+            skip = int(next((a.split("=")[1] for a in sys.argv if a.startswith("--skip=")), "0"))
+            print(sorted(i for i, v in cand if rng[0] <= v <= rng[1])[skip])
         else:
             top = max(v for _, v in cand)
             print(min(i for i, v in cand if v >= 0.95 * top))
