@@ -347,8 +347,14 @@ int choose_splits(std::int64_t m, std::int64_t n, std::int64_t k) {
   const std::int64_t tiles = ((m + BM - 1) / BM) * ((n + BN - 1) / BN);
   const std::int64_t want = 2 * static_cast<std::int64_t>(sm_count());
   std::int64_t s = 1;
-  if (tiles < want && k >= 512) {
-    s = std::min<std::int64_t>((want + tiles - 1) / tiles, k / 256);
+  if (tiles < want && k >= 32) {
+    // Few tiles: split K over idle SMs.  Each K step of this kernel is a
+    // dependent global-load round trip (~2.5 us at one or two CTAs), so the
+    // small side contractions of the Bristlecone plans (m = 16, n = 256,
+    // k = 256: 2 tiles, 80 us) are latency-bound; chunks of >= 16 K there
+    // (>= 256 K on long K, as before).
+    const std::int64_t min_chunk = k >= 512 ? 256 : 2 * BK;
+    s = std::min<std::int64_t>((want + tiles - 1) / tiles, k / min_chunk);
     // Cap the occupancy partial buffer at 1 GiB.
     while (s > 1 && s * m * n * 8 > (std::int64_t{1} << 30)) --s;
   }
