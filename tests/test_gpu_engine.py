@@ -245,13 +245,35 @@ def test_split_handoffs_match_fp32_storage(gpu, monkeypatch):
     assert rel(res["1"], res["0"]) < 5e-6
 
 
-def test_tensor_core_paths_forced_small_vs_oracle(gpu, monkeypatch):
+def test_lane_store_epilogue_matches_staged(gpu, monkeypatch):
+    """The lane-per-row STG.256 split-output epilogue (default) and the staged
+    smem-slab one (QSG_TC_LANESTORE=0) write the same hi | lo planes; on a
+    config-2 slice (13 chained split hand-offs) the amplitudes agree to
+    FP32-level accuracy (only the max |c|^2 bookkeeping is computed
+    differently: on the split values, rescaled once per tile)."""
+    text = gpu.generate_rqc(7, 7, 32, 0)
+    plan = open(os.path.join(ROOT, "configs", "config2_plan.json")).read()
+    x1 = gpu.draw_x1(49, json.loads(plan)["open_qubits"], 0, 1)
+    res = {}
+    for lane in ("1", "0"):
+        monkeypatch.setenv("QSG_TC_LANESTORE", lane)
+        with gpu.Engine(text, plan, tensor_cores=True) as e:
+            e.prepare(x1)
+            e.run([0], reset=True)
+            res[lane] = e.results()
+    assert rel(res["1"], res["0"]) < 1e-6
+
+
+@pytest.mark.parametrize("lane", ["1", "0"])
+def test_tensor_core_paths_forced_small_vs_oracle(gpu, monkeypatch, lane):
     """Forces every supported GEMM onto the tcgen05 path (QSG_TC_MIN_FLOPS=0)
     on a 7x7 (1+20+1) circuit with the config-2 region order and cut, so the
     CTA-pair kernel, its narrow-N variants and the fused output permutation
-    (lookahead layouts) all run at a size the numpy oracle checks exactly."""
+    (lookahead layouts) all run at a size the numpy oracle checks exactly --
+    with the lane-store epilogue and with the staged one."""
     import qsim_oracle as O
     monkeypatch.setenv("QSG_TC_MIN_FLOPS", "0")
+    monkeypatch.setenv("QSG_TC_LANESTORE", lane)
     text = gpu.generate_rqc(7, 7, 20, 0)
     order = json.load(open(os.path.join(ROOT, "configs", "config2_plan.json")))["order"]
     opn = [32, 33, 34, 39, 40, 41, 45, 46, 47, 48]
