@@ -1341,10 +1341,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               // lane's row are one 32-byte run per plane (complex column
               // bits 0..2 are the output's bits 0..2 under the fused
               // permutation; natural order needs n % 8 == 0), written as one
-              // STG.256 per plane straight from registers (its own
-              // instantiation: the staged paths' registers stay out).  The max is kept
-              // on the split values y = acc * 2^-t and rescaled once per tile
-              // (an exact power of two).
+              // STG.256 per plane straight from registers.  Its own
+              // instantiation, so the staged paths' registers stay out.  The
+              // max is kept on the split values y = acc * 2^-t and rescaled
+              // once per tile (an exact power of two).
               const long long row_off =
                   p.store_perm ? my_row_off + col_tile_off
                                : (row_base + lane) * (p.n2 / 2) + (static_cast<long long>(n_tile) * kPairBN + half * HALF) / 2;
