@@ -1971,6 +1971,10 @@ cudaError_t launch_f16_pair(const GemmArgs& g, const TMeta* meta_a, const TMeta*
   const long long pairs = (g.m / 256) * ((2 * g.n) / BN);
   if (pairs >= (1ll << 31)) return cudaErrorInvalidValue;  // pair_tile_coords divides in 32 bits
   p.n_tiles = static_cast<int>((2 * g.n) / BN);
+  // One column tile: no pair shares an A slab with another (B is one small
+  // tile), so K-sync only adds a grid-wide wait every `sync_every` tiles
+  // (config 4's m = 2^27, n = k = 16 steps: -5% without it).
+  if (p.n_tiles == 1) p.sync = nullptr;
   static const long long slots = [] {
     cudaFuncSetAttribute(cgemm_f16_pair_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          Tc5Cfg<BN>::SMEM);
