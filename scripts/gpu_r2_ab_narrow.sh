@@ -1,5 +1,6 @@
 # FP32 streaming kernel for the n = k = 16 split-in / split-out bond-closing steps (QSG_TC_NARROW):
 # GPU tests (full-size Bristlecone parity included), then env A/B on configs 4, 3.
+# (Record of the A/B in profiles/r2/narrow_fp32/: the kernel was removed afterwards, so QSG_TC_NARROW is no longer read.)
 mkdir -p gpurun_out/abnw
 timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_engine.py tests/test_gpu_large.py -m gpu -q -x -p no:cacheprovider > gpurun_out/abnw/pytest.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/abnw/pytest.log
 cp gpurun_out/parity_*.json gpurun_out/abnw/ 2>/dev/null
